@@ -1,0 +1,88 @@
+"""ctypes front-end of the CPU oracle (oracle/_ref/libacs_cpu.so).
+
+TEST INFRASTRUCTURE ONLY — imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs, never by the product path.
+
+The library holds, for every nest function F and form:
+  F__original        the nest text (nests/<nest>.c)            gcc -O3 -ffp-contract=off
+  F__cse|cse_bulk|cse_sat|accsat
+                     the reference-emitted text for that VariantConfig
+                     (tests/golden/emitted/), two-rounding FMA as the
+                     reference interpreter evaluates it (proj/src/interp.cpp:68-70)
+  F__cse_sat_fma|accsat_fma
+                     the same text with each extracted FMA as one fma() —
+                     the arithmetic the sm_100a saturated kernels perform
+  …_f32              (wave4) the textual fp32 copy
+and an ``_omp`` twin of each that splits the outermost loop over threads.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Dict
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_ref", "libacs_cpu.so")
+
+FORM_OF_VARIANT = {"original": "original", "cse": "cse", "cse+bulk": "cse_bulk",
+                   "cse+sat": "cse_sat", "accsat": "accsat"}
+
+_lib = None
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", HERE, "cpu"], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        _lib = ctypes.CDLL(LIB_PATH)
+    return _lib
+
+
+def form_name(variant: str, fma: bool = False, f32: bool = False) -> str:
+    f = FORM_OF_VARIANT[variant]
+    if fma and variant in ("cse+sat", "accsat"):
+        f += "_fma"
+    if f32:
+        f += "_f32"
+    return f
+
+
+def run(spec, arrays: Dict[str, np.ndarray], scalars: Dict[str, float], variant: str = "original",
+        fma: bool = False, f32: bool = False, threads: int = 0) -> None:
+    """Runs one nest function IN PLACE on host arrays (reference layout).
+
+    `spec` is a nests.KernelSpec; `threads` > 0 uses the OpenMP driver."""
+    n = len(spec.params)
+    a = (ctypes.c_void_p * n)()
+    d = (ctypes.c_long * (8 * n))()
+    iv = (ctypes.c_longlong * n)()
+    dv = (ctypes.c_double * n)()
+    for p in spec.params:
+        if p.dims:
+            arr = arrays[p.name]
+            assert arr.flags["C_CONTIGUOUS"], p.name
+            a[p.position] = arr.ctypes.data
+            for k, v in enumerate(arr.shape):
+                d[8 * p.position + k] = v
+        elif p.ctype == "int":
+            iv[p.position] = int(scalars[p.name])
+        else:
+            dv[p.position] = float(scalars[p.name])
+    sym = f"{spec.function}__{form_name(variant, fma, f32)}"
+    if threads > 0:
+        fn = getattr(lib(), sym + "_omp")
+        fn.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int]
+        fn(a, d, iv, dv, threads)
+    else:
+        fn = getattr(lib(), sym)
+        fn.argtypes = [ctypes.c_void_p] * 4
+        fn(a, d, iv, dv)
