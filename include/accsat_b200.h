@@ -1,0 +1,138 @@
+/*
+ * accsat_b200.h — C ABI of the B200 loop-nest execution backend.
+ *
+ * Drop-in boundary for the reference's execution path (arXiv 2306.13002,
+ * ACC Saturator / satcc).  The reference runs a nest either in process with
+ * its interpreter
+ *     Environment eval_region(const Stmt& body, Environment env)
+ *         (proj/include/satcc/interp.hpp:72-74, proj/src/interp.cpp:266-270)
+ * or out of process by handing the emitted C to a compiler
+ *     satcc [flags] -- cc -O3 kernel.c   (proj/tools/satcc_main.cpp:285-360).
+ * This library replaces both with hand-written sm_100a kernels.  Plain C
+ * types only: no C++ types or exceptions cross it.
+ *
+ *   - A kernel is registered under "<file>:<function>:<region index>", the key
+ *     find_regions assigns (proj/src/ast.cpp:390-398, Region::index).
+ *   - A variant is a VariantConfig name (proj/include/satcc/pipeline.hpp:14-20)
+ *     plus ORIGINAL (the unoptimized source text).
+ *   - Arrays are caller-owned DEVICE buffers described like ArrayBuf
+ *     (proj/include/satcc/interp.hpp:27-48): element type, dims, and element
+ *     strides (0 = row-major, i.e. ArrayBuf::flat).  Scalars are named
+ *     int64/double values like Scalar (interp.hpp:13-24).
+ *   - Errors: a status code plus a thread-local message (acs_last_error), the
+ *     analogue of EvalError / InternalError (proj/include/satcc/diag.hpp:43-53).
+ *     There is no CPU fallback: a kernel that is not registered, or a CUDA
+ *     failure, is an error.
+ *   - Launches are asynchronous on the caller's stream; registry lookups are
+ *     thread-safe.
+ */
+#ifndef ACCSAT_B200_H
+#define ACCSAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ACS_ABI_VERSION 1
+#define ACS_MAX_DIMS 8
+
+typedef enum {
+    ACS_OK = 0,
+    ACS_E_ARG = 1,        /* bad argument: null pointer, unknown name, missing array/scalar */
+    ACS_E_NO_KERNEL = 2,  /* kernel id / variant / schedule not registered */
+    ACS_E_SHAPE = 3,      /* dims, strides or dtype do not match the kernel's declaration */
+    ACS_E_CUDA = 4,       /* CUDA runtime error (message has the CUDA error string) */
+    ACS_E_NCCL = 5,       /* peer / collective setup error */
+    ACS_E_BOUNDS = 6      /* iteration space would index outside an array (EvalError analogue) */
+} acs_status;
+
+typedef enum { ACS_F64 = 0, ACS_F32 = 1, ACS_I32 = 2, ACS_I64 = 3, ACS_U8 = 4 } acs_dtype;
+
+/* Forms of a nest: the original source, and the four VariantConfig outputs of
+ * the reference optimizer (pipeline.cpp:97-110). */
+typedef enum {
+    ACS_ORIGINAL = 0,
+    ACS_CSE = 1,
+    ACS_CSE_BULK = 2,
+    ACS_CSE_SAT = 3,
+    ACS_ACCSAT = 4
+} acs_variant;
+
+/* Kernel skeleton: NAIVE = one thread per point, every array reference of the
+ * form is its own global load in source order (what a directive compiler
+ * makes of the text); TILED = the B200 skeleton (shared-memory plane tiles,
+ * register queues along the sweep axis, vectorised streams).  DEFAULT picks
+ * NAIVE for ORIGINAL and the best registered skeleton otherwise. */
+typedef enum { ACS_SCHED_DEFAULT = 0, ACS_SCHED_NAIVE = 1, ACS_SCHED_TILED = 2 } acs_schedule;
+
+typedef struct {
+    const char* name;              /* parameter name in the nest text */
+    acs_dtype dtype;
+    int32_t ndim;
+    int64_t dims[ACS_MAX_DIMS];
+    int64_t strides[ACS_MAX_DIMS]; /* in elements; all zero = row-major (reference layout) */
+    void* data;                    /* device pointer */
+} acs_array;
+
+typedef struct {
+    const char* name;
+    int32_t is_int;                /* 1: use i, 0: use d */
+    int64_t i;
+    double d;
+} acs_scalar;
+
+typedef struct acs_kernel acs_kernel;  /* opaque registry entry */
+
+typedef struct {
+    const char* kernel_id;         /* "<file>:<function>:<region>" */
+    const char* function;
+    int32_t region;
+    int32_t n_loops;               /* marked loops = GPU iteration space */
+    int32_t n_arrays;
+    int32_t n_scalars;
+    int32_t static_loads[5];       /* per acs_variant: array reads per point (count_static_loads) */
+    int32_t fma_count[5];          /* per acs_variant: single-rounding FMAs per point */
+    int32_t has_tiled;             /* a TILED skeleton is registered */
+    int32_t has_f32;               /* an fp32 instantiation is registered */
+} acs_kernel_info;
+
+int acs_abi_version(void);
+const char* acs_last_error(void);
+
+/* Registry (kernel registration by find_regions key). */
+int acs_kernel_count(void);
+const char* acs_kernel_id(int index);
+acs_status acs_lookup(const char* kernel_id, const acs_kernel** out);
+acs_status acs_kernel_get_info(const acs_kernel* k, acs_kernel_info* out);
+const char* acs_kernel_array_name(const acs_kernel* k, int index);
+const char* acs_kernel_scalar_name(const acs_kernel* k, int index);
+int acs_kernel_scalar_is_int(const acs_kernel* k, int index);
+
+/* Runs the WHOLE nest (every marked loop) of one region on `stream`.
+ * Arrays/scalars are matched to the nest's parameters by name. */
+acs_status acs_launch(const acs_kernel* k, acs_variant variant, acs_schedule schedule,
+                      const acs_array* arrays, int n_arrays,
+                      const acs_scalar* scalars, int n_scalars, void* cuda_stream);
+
+/* Device data utilities (synthetic inputs, layout remaps). */
+typedef enum { ACS_FILL_UNIFORM = 0, ACS_FILL_CONST = 1, ACS_FILL_MASK = 2, ACS_FILL_D3Q19 = 3 } acs_fill_kind;
+/* Fills a (possibly strided) array.  Element at reference flat index f gets
+ * SplitMix64(seed, f): UNIFORM lo+(hi-lo)*u, CONST lo, MASK (u < p), D3Q19
+ * w[f % 19] * (1 + (lo+(hi-lo)*u)).  Bit-identical to nests.make_inputs. */
+acs_status acs_fill(const acs_array* a, acs_fill_kind kind, uint64_t seed, double lo, double hi,
+                    double p, void* cuda_stream);
+/* Strided element copy between two arrays of the same dims (any strides,
+ * dtype conversion between integer types or between real types). */
+acs_status acs_copy(const acs_array* dst, const acs_array* src, void* cuda_stream);
+/* Backend-preferred strides for an array of `kernel` (e.g. q-major SoA for the
+ * D3Q19 distribution arrays); row-major otherwise. */
+acs_status acs_native_strides(const acs_kernel* k, const char* array_name, int ndim,
+                              const int64_t* dims, int64_t* strides_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACCSAT_B200_H */

@@ -1,0 +1,272 @@
+"""Host-side mirror of the reference's execution API over the C ABI.
+
+``eval_region`` here is the drop-in for the reference's
+
+    Environment eval_region(const Stmt& body, Environment env)
+        (proj/include/satcc/interp.hpp:72-74, proj/src/interp.cpp:266-270)
+
+with the same value semantics — the environment is copied in and a new one
+returned — except that it executes the WHOLE nest of one registered region on
+the B200 (libaccsat_b200.so, include/accsat_b200.h) instead of tree-walking
+it.  Errors map to the reference's exception types: ``EvalError`` for
+runtime failures (bounds, missing names — proj/include/satcc/diag.hpp:43-47),
+``InternalError`` for broken invariants (diag.hpp:50-53).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device
+is visible, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libaccsat_b200.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "accsat_b200.h")
+
+ACS_OK, ACS_E_ARG, ACS_E_NO_KERNEL, ACS_E_SHAPE, ACS_E_CUDA, ACS_E_NCCL, ACS_E_BOUNDS = range(7)
+F64, F32, I32, I64, U8 = range(5)
+VARIANTS = {"original": 0, "cse": 1, "cse+bulk": 2, "cse+sat": 3, "accsat": 4}
+SCHEDULES = {"default": 0, "naive": 1, "tiled": 2}
+FILL = {"uniform": 0, "const": 1, "mask": 2, "d3q19": 3}
+MAX_DIMS = 8
+
+
+class EvalError(RuntimeError):
+    """Runtime failure of a nest (satcc::EvalError analogue)."""
+
+
+class InternalError(RuntimeError):
+    """Broken invariant / backend failure (satcc::InternalError analogue)."""
+
+
+class AcsArray(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("dtype", ctypes.c_int), ("ndim", ctypes.c_int32),
+                ("dims", ctypes.c_int64 * MAX_DIMS), ("strides", ctypes.c_int64 * MAX_DIMS),
+                ("data", ctypes.c_void_p)]
+
+
+class AcsScalar(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("is_int", ctypes.c_int32), ("i", ctypes.c_int64),
+                ("d", ctypes.c_double)]
+
+
+class AcsKernelInfo(ctypes.Structure):
+    _fields_ = [("kernel_id", ctypes.c_char_p), ("function", ctypes.c_char_p), ("region", ctypes.c_int32),
+                ("n_loops", ctypes.c_int32), ("n_arrays", ctypes.c_int32), ("n_scalars", ctypes.c_int32),
+                ("static_loads", ctypes.c_int32 * 5), ("fma_count", ctypes.c_int32 * 5),
+                ("has_tiled", ctypes.c_int32), ("has_f32", ctypes.c_int32)]
+
+
+EXPORTS = {
+    "acs_abi_version": (ctypes.c_int, []),
+    "acs_last_error": (ctypes.c_char_p, []),
+    "acs_kernel_count": (ctypes.c_int, []),
+    "acs_kernel_id": (ctypes.c_char_p, [ctypes.c_int]),
+    "acs_lookup": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "acs_kernel_get_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(AcsKernelInfo)]),
+    "acs_kernel_array_name": (ctypes.c_char_p, [ctypes.c_void_p, ctypes.c_int]),
+    "acs_kernel_scalar_name": (ctypes.c_char_p, [ctypes.c_void_p, ctypes.c_int]),
+    "acs_kernel_scalar_is_int": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "acs_launch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(AcsArray),
+                                  ctypes.c_int, ctypes.POINTER(AcsScalar), ctypes.c_int, ctypes.c_void_p]),
+    "acs_fill": (ctypes.c_int, [ctypes.POINTER(AcsArray), ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
+                                ctypes.c_double, ctypes.c_double, ctypes.c_void_p]),
+    "acs_copy": (ctypes.c_int, [ctypes.POINTER(AcsArray), ctypes.POINTER(AcsArray), ctypes.c_void_p]),
+    "acs_native_strides": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
+}
+
+_lib = None
+
+
+def lib():
+    """The loaded backend.  Raises if the sm_100a library was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise InternalError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                                "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in EXPORTS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str) -> None:
+    if status == ACS_OK:
+        return
+    msg = lib().acs_last_error().decode()
+    if status in (ACS_E_BOUNDS, ACS_E_ARG, ACS_E_SHAPE, ACS_E_NO_KERNEL):
+        raise EvalError(f"{what}: {msg}")
+    raise InternalError(f"{what}: {msg}")
+
+
+def kernel_ids():
+    L = lib()
+    return [L.acs_kernel_id(i).decode() for i in range(L.acs_kernel_count())]
+
+
+# ---------------------------------------------------------------------------
+# tensors <-> descriptors (torch is used for device memory and streams only)
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    m = {torch.float64: F64, torch.float32: F32, torch.int32: I32, torch.int64: I64, torch.uint8: U8}
+    return m[t.dtype]
+
+
+def describe(name: str, t) -> AcsArray:
+    """acs_array for a torch CUDA tensor (any strides)."""
+    a = AcsArray()
+    a.name = name.encode()
+    a.dtype = _dtype_code(t)
+    a.ndim = t.dim()
+    for p in range(t.dim()):
+        a.dims[p] = t.shape[p]
+        a.strides[p] = t.stride(p)
+    a.data = t.data_ptr()
+    return a
+
+
+def _stream_handle(stream) -> Optional[int]:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+@dataclass
+class Kernel:
+    """One registered region (a C-ABI acs_kernel handle)."""
+    kernel_id: str
+    handle: int
+    info: Dict = field(default_factory=dict)
+
+    @classmethod
+    def lookup(cls, kernel_id: str) -> "Kernel":
+        h = ctypes.c_void_p()
+        _check(lib().acs_lookup(kernel_id.encode(), ctypes.byref(h)), "acs_lookup")
+        inf = AcsKernelInfo()
+        _check(lib().acs_kernel_get_info(h, ctypes.byref(inf)), "acs_kernel_get_info")
+        info = {"function": inf.function.decode(), "region": inf.region, "n_loops": inf.n_loops,
+                "static_loads": list(inf.static_loads), "fma_count": list(inf.fma_count),
+                "has_tiled": bool(inf.has_tiled), "has_f32": bool(inf.has_f32),
+                "arrays": [lib().acs_kernel_array_name(h, i).decode() for i in range(inf.n_arrays)],
+                "scalars": [lib().acs_kernel_scalar_name(h, i).decode() for i in range(inf.n_scalars)],
+                "scalar_is_int": [lib().acs_kernel_scalar_is_int(h, i) for i in range(inf.n_scalars)]}
+        return cls(kernel_id, h.value, info)
+
+    def launch(self, arrays: Dict[str, object], scalars: Dict[str, float], variant: str = "accsat",
+               schedule: str = "default", stream=None) -> None:
+        """Asynchronous launch on `stream` (torch stream; default current)."""
+        descs = (AcsArray * len(arrays))(*[describe(n, t) for n, t in arrays.items()])
+        sc = (AcsScalar * len(scalars))()
+        for i, (n, v) in enumerate(scalars.items()):
+            sc[i].name = n.encode()
+            is_int = isinstance(v, (int, np.integer)) and not isinstance(v, bool)
+            sc[i].is_int = 1 if is_int else 0
+            sc[i].i = int(v) if is_int else 0
+            sc[i].d = float(v)
+        _check(lib().acs_launch(self.handle, VARIANTS[variant], SCHEDULES[schedule], descs, len(arrays), sc,
+                                len(scalars), _stream_handle(stream)), f"acs_launch({self.kernel_id}, {variant})")
+
+    def native_strides(self, name: str, dims: Tuple[int, ...]) -> Tuple[int, ...]:
+        d = (ctypes.c_int64 * len(dims))(*dims)
+        s = (ctypes.c_int64 * len(dims))()
+        _check(lib().acs_native_strides(self.handle, name.encode(), len(dims), d, s), "acs_native_strides")
+        return tuple(s)
+
+
+def fill(t, kind: str, seed: int, lo: float = 0.0, hi: float = 1.0, p: float = 0.0, stream=None) -> None:
+    a = describe("fill", t)
+    _check(lib().acs_fill(ctypes.byref(a), FILL[kind], seed, lo, hi, p, _stream_handle(stream)), "acs_fill")
+
+
+def copy(dst, src, stream=None) -> None:
+    a, b = describe("dst", dst), describe("src", src)
+    _check(lib().acs_copy(ctypes.byref(a), ctypes.byref(b), _stream_handle(stream)), "acs_copy")
+
+
+def empty_native(kernel: Kernel, name: str, dims, dtype, device="cuda"):
+    """Device tensor with the backend's preferred strides for `name`."""
+    torch = _torch()
+    st = kernel.native_strides(name, tuple(dims))
+    n = int(np.prod(dims))
+    return torch.empty_strided(tuple(dims), st, dtype=dtype, device=device) if n else \
+        torch.empty(tuple(dims), dtype=dtype, device=device)
+
+
+# ---------------------------------------------------------------------------
+# Environment / eval_region mirror
+
+@dataclass
+class Environment:
+    """Name-keyed state (satcc::Environment, proj/include/satcc/interp.hpp:51-54):
+    host numpy arrays (reference row-major layout) and Python scalars."""
+    scalars: Dict[str, float] = field(default_factory=dict)
+    arrays: Dict[str, np.ndarray] = field(default_factory=dict)
+
+    def copy(self) -> "Environment":
+        return Environment(dict(self.scalars), {k: v.copy() for k, v in self.arrays.items()})
+
+
+_NP2TORCH = None
+
+
+def _to_device(a: np.ndarray, kernel: Kernel, name: str, native: bool):
+    torch = _torch()
+    host = torch.from_numpy(np.ascontiguousarray(a))
+    if not native:
+        return host.to("cuda", non_blocking=False)
+    dev_rm = host.to("cuda")
+    st = kernel.native_strides(name, tuple(a.shape))
+    rm = tuple(dev_rm.stride())
+    if st == rm:
+        return dev_rm
+    dev = torch.empty_strided(tuple(a.shape), st, dtype=dev_rm.dtype, device="cuda")
+    copy(dev, dev_rm)
+    return dev
+
+
+def eval_region(kernel_id: str, env: Environment, variant: str = "accsat", schedule: str = "default",
+                native_layout: bool = True) -> Environment:
+    """Runs the whole nest of `kernel_id` on the B200 over a copy of `env`
+    and returns the post-state (value semantics, like satcc::eval_region)."""
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise InternalError("no CUDA device visible: the B200 backend has no CPU fallback")
+    k = Kernel.lookup(kernel_id)
+    dev = {}
+    for name in k.info["arrays"]:
+        if name not in env.arrays:
+            raise EvalError(f"read of undefined array: {name}")
+        dev[name] = _to_device(env.arrays[name], k, name, native_layout)
+    sc = {}
+    for name, is_int in zip(k.info["scalars"], k.info["scalar_is_int"]):
+        if name not in env.scalars:
+            raise EvalError(f"read of undefined variable: {name}")
+        v = env.scalars[name]
+        sc[name] = int(v) if is_int else float(v)
+    k.launch(dev, sc, variant, schedule)
+    out = env.copy()
+    for name, t in dev.items():
+        if t.is_contiguous():
+            out.arrays[name] = t.cpu().numpy()
+        else:
+            rm = torch.empty(t.shape, dtype=t.dtype, device="cuda")
+            copy(rm, t)
+            out.arrays[name] = rm.cpu().numpy()
+    torch.cuda.synchronize()
+    return out

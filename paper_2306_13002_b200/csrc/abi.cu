@@ -1,0 +1,324 @@
+// abi.cu — the C ABI (include/accsat_b200.h): registry, launch dispatch,
+// error reporting and the device data utilities (seeded fills, strided copies).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "registry.hpp"
+
+namespace acs {
+
+void register_jacobi7();
+void register_swim();
+void register_clover();
+void register_wave4();
+void register_d3q19();
+
+namespace {
+thread_local std::string g_err;
+std::vector<Entry*>& registry() {
+    static std::vector<Entry*> r;
+    return r;
+}
+std::once_flag g_once;
+void init_registry() {
+    std::call_once(g_once, [] {
+        register_jacobi7();
+        register_swim();
+        register_clover();
+        register_wave4();
+        register_d3q19();
+    });
+}
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+void register_entry(Entry* e) { registry().push_back(e); }
+Entry* find_entry(const std::string& id) {
+    for (Entry* e : registry())
+        if (e->kernel_id == id) return e;
+    return nullptr;
+}
+
+// ---- seeded fills: the device twin of nests.make_inputs ---------------------
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t seed, uint64_t idx) {
+    uint64_t z = seed + (idx + 1ULL) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+struct StridedDesc {
+    int ndim;
+    long long dims[8];
+    long long stride[8];
+};
+
+__device__ __forceinline__ long long strided_offset(const StridedDesc& d, long long flat) {
+    long long off = 0;
+    for (int p = d.ndim - 1; p >= 0; --p) {
+        const long long ip = flat % d.dims[p];
+        flat /= d.dims[p];
+        off += ip * d.stride[p];
+    }
+    return off;
+}
+
+template <class T>
+__global__ void fill_kernel(T* base, StridedDesc d, long long n, int kind, uint64_t seed, double lo, double hi,
+                            double p) {
+    const double span = __dsub_rn(hi, lo);
+    const double w[3] = {1.0 / 3.0, 1.0 / 18.0, 1.0 / 36.0};
+    for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < n; f += (long long)gridDim.x * blockDim.x) {
+        double v;
+        if (kind == ACS_FILL_CONST) {
+            v = lo;
+        } else {
+            const double u = (double)(splitmix64(seed, (uint64_t)f) >> 11) * 0x1.0p-53;
+            if (kind == ACS_FILL_MASK) {
+                v = u < p ? 1.0 : 0.0;
+            } else {
+                const double x = __dadd_rn(lo, __dmul_rn(span, u));
+                if (kind == ACS_FILL_D3Q19) {
+                    const int q = (int)(f % 19);
+                    v = __dmul_rn(w[q == 0 ? 0 : (q <= 6 ? 1 : 2)], __dadd_rn(1.0, x));
+                } else {
+                    v = x;
+                }
+            }
+        }
+        base[strided_offset(d, f)] = (T)v;
+    }
+}
+
+template <>
+__global__ void fill_kernel<float>(float* base, StridedDesc d, long long n, int kind, uint64_t seed, double lo,
+                                   double hi, double p) {
+    const double span = __dsub_rn(hi, lo);
+    const double w[3] = {1.0 / 3.0, 1.0 / 18.0, 1.0 / 36.0};
+    for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < n; f += (long long)gridDim.x * blockDim.x) {
+        double v;
+        if (kind == ACS_FILL_CONST) {
+            v = lo;
+        } else {
+            const double u = (double)(splitmix64(seed, (uint64_t)f) >> 11) * 0x1.0p-53;
+            const double x = __dadd_rn(lo, __dmul_rn(span, u));
+            v = kind == ACS_FILL_MASK ? (u < p ? 1.0 : 0.0)
+                : kind == ACS_FILL_D3Q19 ? __dmul_rn(w[(f % 19) == 0 ? 0 : ((f % 19) <= 6 ? 1 : 2)], __dadd_rn(1.0, x))
+                : x;
+        }
+        base[strided_offset(d, f)] = __double2float_rn(v);
+    }
+}
+
+template <class D, class S>
+__global__ void copy_kernel(D* dst, StridedDesc dd, const S* src, StridedDesc sd, long long n) {
+    for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < n; f += (long long)gridDim.x * blockDim.x)
+        dst[strided_offset(dd, f)] = (D)src[strided_offset(sd, f)];
+}
+
+namespace {
+
+bool make_desc(const acs_array* a, StridedDesc& d, long long& n) {
+    if (!a || a->ndim < 1 || a->ndim > 8 || !a->data) return false;
+    d.ndim = a->ndim;
+    bool rowmajor = true;
+    for (int p = 0; p < a->ndim; ++p) {
+        if (a->dims[p] <= 0) return false;
+        d.dims[p] = a->dims[p];
+        if (a->strides[p] != 0) rowmajor = false;
+    }
+    long long st = 1;
+    for (int p = a->ndim - 1; p >= 0; --p) {
+        d.stride[p] = rowmajor ? st : a->strides[p];
+        st *= a->dims[p];
+    }
+    n = st;
+    return true;
+}
+
+int grid_for(long long n) {
+    long long g = (n + 255) / 256;
+    const long long cap = 148LL * 16;  // persistent-ish: 16 CTAs per SM, grid-stride
+    return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
+}
+
+}  // namespace
+}  // namespace acs
+
+using namespace acs;
+
+extern "C" {
+
+int acs_abi_version(void) { return ACS_ABI_VERSION; }
+const char* acs_last_error(void) { return g_err.c_str(); }
+
+int acs_kernel_count(void) {
+    init_registry();
+    return (int)registry().size();
+}
+
+const char* acs_kernel_id(int index) {
+    init_registry();
+    if (index < 0 || index >= (int)registry().size()) return nullptr;
+    return registry()[index]->kernel_id.c_str();
+}
+
+acs_status acs_lookup(const char* kernel_id, const acs_kernel** out) {
+    init_registry();
+    if (!kernel_id || !out) {
+        set_error("acs_lookup: null argument");
+        return ACS_E_ARG;
+    }
+    Entry* e = find_entry(kernel_id);
+    if (!e) {
+        set_error(std::string("no kernel registered for '") + kernel_id + "'");
+        return ACS_E_NO_KERNEL;
+    }
+    *out = reinterpret_cast<const acs_kernel*>(e);
+    return ACS_OK;
+}
+
+acs_status acs_kernel_get_info(const acs_kernel* k, acs_kernel_info* out) {
+    if (!k || !out) {
+        set_error("acs_kernel_get_info: null argument");
+        return ACS_E_ARG;
+    }
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    out->kernel_id = e->kernel_id.c_str();
+    out->function = e->function.c_str();
+    out->region = e->region;
+    out->n_loops = e->n_loops;
+    out->n_arrays = (int)e->arrays.size();
+    out->n_scalars = (int)e->scalars.size();
+    for (int v = 0; v < 5; ++v) {
+        out->static_loads[v] = e->static_loads[v];
+        out->fma_count[v] = e->fma_count[v];
+    }
+    out->has_tiled = e->launch[0][ACS_ACCSAT][1] != nullptr;
+    out->has_f32 = e->launch[1][0][0] != nullptr;
+    return ACS_OK;
+}
+
+const char* acs_kernel_array_name(const acs_kernel* k, int index) {
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    if (!e || index < 0 || index >= (int)e->arrays.size()) return nullptr;
+    return e->arrays[index].c_str();
+}
+const char* acs_kernel_scalar_name(const acs_kernel* k, int index) {
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    if (!e || index < 0 || index >= (int)e->scalars.size()) return nullptr;
+    return e->scalars[index].c_str();
+}
+int acs_kernel_scalar_is_int(const acs_kernel* k, int index) {
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    if (!e || index < 0 || index >= (int)e->scalars.size()) return -1;
+    return e->scalar_is_int[index];
+}
+
+acs_status acs_launch(const acs_kernel* k, acs_variant variant, acs_schedule schedule, const acs_array* arrays,
+                      int n_arrays, const acs_scalar* scalars, int n_scalars, void* cuda_stream) {
+    if (!k || (n_arrays > 0 && !arrays) || (n_scalars > 0 && !scalars)) {
+        set_error("acs_launch: null argument");
+        return ACS_E_ARG;
+    }
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    if ((int)variant < 0 || (int)variant > 4) {
+        set_error("acs_launch: unknown variant");
+        return ACS_E_ARG;
+    }
+    // precision from the first real-typed array argument
+    int prec = 0;
+    for (int i = 0; i < n_arrays; ++i)
+        if (arrays[i].dtype == ACS_F32) prec = 1;
+    int sched;
+    if (schedule == ACS_SCHED_DEFAULT)
+        sched = (variant != ACS_ORIGINAL && e->launch[prec][variant][1]) ? 1 : 0;
+    else
+        sched = schedule == ACS_SCHED_TILED ? 1 : 0;
+    LaunchFn fn = e->launch[prec][variant][sched];
+    if (!fn) {
+        set_error(e->kernel_id + ": no " + (sched ? "tiled" : "naive") + " kernel for variant " +
+                  std::to_string(variant) + (prec ? " (fp32)" : ""));
+        return ACS_E_NO_KERNEL;
+    }
+    LaunchReq r{arrays, n_arrays, scalars, n_scalars, static_cast<cudaStream_t>(cuda_stream)};
+    return fn(r);
+}
+
+acs_status acs_fill(const acs_array* a, acs_fill_kind kind, uint64_t seed, double lo, double hi, double p,
+                    void* cuda_stream) {
+    StridedDesc d;
+    long long n;
+    if (!make_desc(a, d, n)) {
+        set_error("acs_fill: bad array descriptor");
+        return ACS_E_ARG;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const int g = grid_for(n);
+    switch (a->dtype) {
+        case ACS_F64: fill_kernel<double><<<g, 256, 0, s>>>((double*)a->data, d, n, kind, seed, lo, hi, p); break;
+        case ACS_F32: fill_kernel<float><<<g, 256, 0, s>>>((float*)a->data, d, n, kind, seed, lo, hi, p); break;
+        case ACS_I32: fill_kernel<int><<<g, 256, 0, s>>>((int*)a->data, d, n, kind, seed, lo, hi, p); break;
+        case ACS_U8: fill_kernel<uint8_t><<<g, 256, 0, s>>>((uint8_t*)a->data, d, n, kind, seed, lo, hi, p); break;
+        default: set_error("acs_fill: unsupported dtype"); return ACS_E_ARG;
+    }
+    return check_launch("acs_fill");
+}
+
+acs_status acs_copy(const acs_array* dst, const acs_array* src, void* cuda_stream) {
+    StridedDesc dd, sd;
+    long long nd, ns;
+    if (!make_desc(dst, dd, nd) || !make_desc(src, sd, ns) || dst->ndim != src->ndim) {
+        set_error("acs_copy: bad array descriptor");
+        return ACS_E_ARG;
+    }
+    for (int p = 0; p < dst->ndim; ++p)
+        if (dst->dims[p] != src->dims[p]) {
+            set_error("acs_copy: dims differ");
+            return ACS_E_SHAPE;
+        }
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const int g = grid_for(nd);
+    const acs_dtype a = dst->dtype, b = src->dtype;
+    if (a == ACS_F64 && b == ACS_F64) copy_kernel<double, double><<<g, 256, 0, s>>>((double*)dst->data, dd, (const double*)src->data, sd, nd);
+    else if (a == ACS_F32 && b == ACS_F32) copy_kernel<float, float><<<g, 256, 0, s>>>((float*)dst->data, dd, (const float*)src->data, sd, nd);
+    else if (a == ACS_I32 && b == ACS_I32) copy_kernel<int, int><<<g, 256, 0, s>>>((int*)dst->data, dd, (const int*)src->data, sd, nd);
+    else if (a == ACS_U8 && b == ACS_I32) copy_kernel<uint8_t, int><<<g, 256, 0, s>>>((uint8_t*)dst->data, dd, (const int*)src->data, sd, nd);
+    else if (a == ACS_I32 && b == ACS_U8) copy_kernel<int, uint8_t><<<g, 256, 0, s>>>((int*)dst->data, dd, (const uint8_t*)src->data, sd, nd);
+    else {
+        set_error("acs_copy: unsupported dtype pair");
+        return ACS_E_ARG;
+    }
+    return check_launch("acs_copy");
+}
+
+acs_status acs_native_strides(const acs_kernel* k, const char* array_name, int ndim, const int64_t* dims,
+                              int64_t* strides_out) {
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    if (!e || !array_name || !dims || !strides_out || ndim < 1 || ndim > 8) {
+        set_error("acs_native_strides: bad argument");
+        return ACS_E_ARG;
+    }
+    int64_t st = 1;
+    for (int p = ndim - 1; p >= 0; --p) {
+        strides_out[p] = st;
+        st *= dims[p];
+    }
+    if (e->soa_last_dim && ndim >= 2 && std::string(array_name) != "flags") {
+        // q-major SoA: the trailing (distribution) subscript becomes the slowest.
+        int64_t cell = 1;
+        for (int p = ndim - 2; p >= 0; --p) {
+            strides_out[p] = cell;
+            cell *= dims[p];
+        }
+        strides_out[ndim - 1] = cell;
+    }
+    return ACS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,34 @@
+// Registration of the clover nest functions (generated bodies: gen/clover.cuh).
+#include "registry.hpp"
+#include "gen/clover.cuh"
+
+namespace acs {
+
+void register_clover() {
+    {
+        static Entry e;
+        e.kernel_id = "clover.c:ideal_gas:0";
+        e.function = "ideal_gas";
+        describe<gen::ideal_gas>(e, "clover.c", 0);
+        fill_naive<gen::ideal_gas, double>(e, 0);
+        register_entry(&e);
+    }
+    {
+        static Entry e;
+        e.kernel_id = "clover.c:pdv_predict:1";
+        e.function = "pdv_predict";
+        describe<gen::pdv_predict>(e, "clover.c", 1);
+        fill_naive<gen::pdv_predict, double>(e, 0);
+        register_entry(&e);
+    }
+    {
+        static Entry e;
+        e.kernel_id = "clover.c:advec_cell_x:2";
+        e.function = "advec_cell_x";
+        describe<gen::advec_cell_x>(e, "clover.c", 2);
+        fill_naive<gen::advec_cell_x, double>(e, 0);
+        register_entry(&e);
+    }
+}
+
+}  // namespace acs

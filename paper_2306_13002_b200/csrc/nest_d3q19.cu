@@ -1,0 +1,19 @@
+// Registration of the d3q19 nest functions (generated bodies: gen/d3q19.cuh).
+#include "registry.hpp"
+#include "gen/d3q19.cuh"
+
+namespace acs {
+
+void register_d3q19() {
+    {
+        static Entry e;
+        e.kernel_id = "d3q19.c:stream_collide:0";
+        e.function = "stream_collide";
+        describe<gen::stream_collide>(e, "d3q19.c", 0);
+        fill_naive<gen::stream_collide, double>(e, 0);
+        e.soa_last_dim = true;
+        register_entry(&e);
+    }
+}
+
+}  // namespace acs

@@ -1,0 +1,18 @@
+// Registration of the jacobi7 nest functions (generated bodies: gen/jacobi7.cuh).
+#include "registry.hpp"
+#include "gen/jacobi7.cuh"
+
+namespace acs {
+
+void register_jacobi7() {
+    {
+        static Entry e;
+        e.kernel_id = "jacobi7.c:jacobi7:0";
+        e.function = "jacobi7";
+        describe<gen::jacobi7>(e, "jacobi7.c", 0);
+        fill_naive<gen::jacobi7, double>(e, 0);
+        register_entry(&e);
+    }
+}
+
+}  // namespace acs

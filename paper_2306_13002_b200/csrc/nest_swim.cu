@@ -1,0 +1,34 @@
+// Registration of the swim nest functions (generated bodies: gen/swim.cuh).
+#include "registry.hpp"
+#include "gen/swim.cuh"
+
+namespace acs {
+
+void register_swim() {
+    {
+        static Entry e;
+        e.kernel_id = "swim.c:calc1:0";
+        e.function = "calc1";
+        describe<gen::calc1>(e, "swim.c", 0);
+        fill_naive<gen::calc1, double>(e, 0);
+        register_entry(&e);
+    }
+    {
+        static Entry e;
+        e.kernel_id = "swim.c:calc2:1";
+        e.function = "calc2";
+        describe<gen::calc2>(e, "swim.c", 1);
+        fill_naive<gen::calc2, double>(e, 0);
+        register_entry(&e);
+    }
+    {
+        static Entry e;
+        e.kernel_id = "swim.c:calc3:2";
+        e.function = "calc3";
+        describe<gen::calc3>(e, "swim.c", 2);
+        fill_naive<gen::calc3, double>(e, 0);
+        register_entry(&e);
+    }
+}
+
+}  // namespace acs

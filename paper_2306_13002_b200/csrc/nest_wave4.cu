@@ -1,0 +1,19 @@
+// Registration of the wave4 nest functions (generated bodies: gen/wave4.cuh).
+#include "registry.hpp"
+#include "gen/wave4.cuh"
+
+namespace acs {
+
+void register_wave4() {
+    {
+        static Entry e;
+        e.kernel_id = "wave4.c:wave4:0";
+        e.function = "wave4";
+        describe<gen::wave4>(e, "wave4.c", 0);
+        fill_naive<gen::wave4, double>(e, 0);
+        fill_naive<gen::wave4_f32, float>(e, 1);
+        register_entry(&e);
+    }
+}
+
+}  // namespace acs

@@ -1,0 +1,548 @@
+"""Lowers a nest function (kernel-subset C) to sm_100a device code.
+
+This is the backend's compile stage for the execution path: it takes a nest
+text — the ORIGINAL source (nests/<nest>.c) or a form EMITTED by the
+reference optimizer (tests/golden/emitted/<nest>.<variant>.c, the
+``optimize_source`` output of proj/src/pipeline.cpp:140-194) — and produces,
+per registered region, a ``__device__`` per-point body.  The hand-written
+kernel skeletons (csrc/kernels/*.cuh) decide the thread mapping and where each
+array element comes from (global memory, a shared-memory tile, a register
+queue, a warp shuffle); the body only names *which* element it needs.
+
+Arithmetic is emitted with explicit IEEE round-to-nearest intrinsics so the
+result never depends on nvcc's contraction choices:
+
+* every ``+ - * /`` of the text is one rounding (``__dadd_rn`` …), in the
+  text's evaluation order (C left-to-right, proj/src/printer.cpp precedence);
+* in the saturated forms every extracted FMA temp ``_vN = a + b * c``
+  (an ``Fma`` node, printed by proj/src/printer.cpp:114-125) becomes ONE
+  ``__fma_rn(b, c, a)`` — the hardware FMA the paper's rules introduce
+  (FMA1-3, proj/src/rules.cpp:129-135);
+* C semantics of the reference interpreter otherwise (apply_bin/apply_un/
+  apply_call/coerce, proj/src/interp.cpp:24-112): int∘int stays int with
+  truncating ``/ %``, mixed operands promote to double, comparisons yield int,
+  assignments coerce to the target type, sqrt is correctly rounded.
+
+Loads: each array reference becomes ``m.template ld<ARR, o...>()`` when every
+subscript is (loop variable + constant) or a constant — resolved through the
+single-assignment ``_v`` int temps the emitter introduces (``_v4 = k + 1``) —
+and ``m.template ldx<ARR>(idx...)`` otherwise (data-dependent donor/upwind
+indices).  Stores likewise (``st`` / ``stx``).  In the ORIGINAL form the
+skeleton issues one real global load per reference, in source order; in the
+saturated forms loads are the CSE'd set the extraction kept.
+"""
+from __future__ import annotations
+
+import os
+import re
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
+
+from . import kernel_subset as ks
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+LIBM1 = {"sqrt", "fabs", "sin", "cos", "exp", "log", "floor", "ceil"}
+LIBM2 = {"pow", "fmin", "fmax"}
+
+
+@dataclass
+class Affine:
+    var: Optional[str]   # loop variable, or None for a constant
+    off: int
+
+
+@dataclass
+class Lowered:
+    function: str
+    params: List[ks.Param]
+    loop_vars: List[str]
+    bounds: List[Tuple[str, str]]             # per loop: (lo expr, hi expr), half-open, device C
+    sig: Dict[str, List[int]]                 # array -> per position loop index / -1 absolute
+    stored: set
+    body: str                                 # device function body text
+    n_fma: int = 0
+    n_loads: int = 0
+    n_dyn_loads: int = 0
+    offrange: Dict[str, List[List[int]]] = field(default_factory=dict)
+
+
+class LowerError(Exception):
+    pass
+
+
+class _Lowerer:
+    def __init__(self, fn: ks.Function, region: ks.Region, fma: bool, f32: bool):
+        self.fn = fn
+        self.region = region
+        self.fma = fma
+        self.f32 = f32
+        self.types: Dict[str, str] = {}        # scalar name -> int|double
+        self.arrays: Dict[str, ks.Param] = {}
+        for p in fn.params:
+            if p.dims:
+                self.arrays[p.name] = p
+            else:
+                self.types[p.name] = p.ty
+        self.loop_vars = [l.loop_var for l in region.marked_loops]
+        if len(region.marked_loops) != len(region.loops):
+            raise LowerError(f"{fn.name}: unmarked loops enclosing the region are not supported")
+        for v in self.loop_vars:
+            self.types[v] = "int"
+        self.affine: Dict[str, Affine] = {v: Affine(v, 0) for v in self.loop_vars}
+        self.assign_count: Dict[str, int] = {}
+        self.sig: Dict[str, List[Optional[int]]] = {}
+        self.offrange: Dict[str, List[List[int]]] = {}
+        self.stored = set()
+        self.n_fma = self.n_loads = self.n_dyn = 0
+
+    # -- types
+    def real(self) -> str:
+        return "float" if self.f32 else "double"
+
+    def expr_type(self, e: ks.Expr) -> str:
+        if e.kind == "int":
+            return "int"
+        if e.kind == "float":
+            return "double"
+        if e.kind == "var":
+            if e.op not in self.types:
+                raise LowerError(f"undeclared scalar {e.op}")
+            return self.types[e.op]
+        if e.kind == "ref":
+            return "int" if self.arrays[e.op].ty == "int" else "double"
+        if e.kind == "call":
+            return "double"
+        if e.kind == "un":
+            return "int" if e.op == "!" else self.expr_type(e.kids[0])
+        if e.op in ("<", "<=", ">", ">=", "==", "!=", "&&", "||"):
+            return "int"
+        a, b = self.expr_type(e.kids[0]), self.expr_type(e.kids[1])
+        return "int" if a == b == "int" else "double"
+
+    # -- affine resolution of subscripts
+    def count_assigns(self, s: ks.Stmt):
+        if s.kind == "assign" and s.lhs.kind == "var":
+            self.assign_count[s.lhs.op] = self.assign_count.get(s.lhs.op, 0) + 1
+        for c in ks.children(s):
+            self.count_assigns(c)
+
+    def as_affine(self, e: ks.Expr) -> Optional[Affine]:
+        if e.kind == "int":
+            return Affine(None, int(e.text))
+        if e.kind == "var":
+            return self.affine.get(e.op)
+        if e.kind == "bin" and e.op in ("+", "-"):
+            a, b = self.as_affine(e.kids[0]), self.as_affine(e.kids[1])
+            if a is None or b is None:
+                return None
+            if e.op == "+" and (a.var is None or b.var is None):
+                return Affine(a.var or b.var, a.off + b.off)
+            if e.op == "-" and b.var is None:
+                return Affine(a.var, a.off - b.off)
+        return None
+
+    def ref_offsets(self, e: ks.Expr) -> Optional[List[int]]:
+        arr = e.op
+        offs, sig = [], []
+        for idx in e.kids:
+            a = self.as_affine(idx)
+            if a is None:
+                return None
+            sig.append(self.loop_vars.index(a.var) if a.var is not None else -1)
+            offs.append(a.off)
+        known = self.sig.get(arr)
+        if known is None:
+            self.sig[arr] = sig
+        elif known != sig:
+            return None        # inconsistent position mapping: go dynamic
+        rng = self.offrange.setdefault(arr, [[o, o] for o in offs])
+        for p, o in enumerate(offs):
+            rng[p][0] = min(rng[p][0], o)
+            rng[p][1] = max(rng[p][1], o)
+        return offs
+
+    # -- expressions
+    def lit(self, e: ks.Expr) -> str:
+        t = e.text.rstrip("fF")
+        if self.f32:
+            return t + "f" if ("." in t or "e" in t or "E" in t) else t
+        return t
+
+    def conv(self, code: str, have: str, want: str) -> str:
+        if have == want:
+            return code
+        if want == "double":
+            return f"(({self.real()})({code}))"
+        return f"((int)({code}))"
+
+    def ex(self, e: ks.Expr) -> Tuple[str, str]:
+        k = e.kind
+        if k == "int":
+            return e.text, "int"
+        if k == "float":
+            return self.lit(e), "double"
+        if k == "var":
+            return e.op, self.types[e.op]
+        if k == "ref":
+            return self.load(e), ("int" if self.arrays[e.op].ty == "int" else "double")
+        if k == "call":
+            return self.call(e), "double"
+        if k == "un":
+            c, t = self.ex(e.kids[0])
+            if e.op == "!":
+                return f"(!({c}))", "int"
+            return f"(-({c}))", t
+        op = e.op
+        if op in ("&&", "||"):
+            a, _ = self.ex(e.kids[0])
+            b, _ = self.ex(e.kids[1])
+            return f"(({a}) {op} ({b}))", "int"
+        a, ta = self.ex(e.kids[0])
+        b, tb = self.ex(e.kids[1])
+        if ta == tb == "int":
+            if op in ("/", "%"):
+                # C truncation semantics (interp: int /0 and %0 are EvalErrors)
+                return f"(({a}) {op} ({b}))", "int"
+            return f"(({a}) {op} ({b}))", "int"
+        a, b = self.conv(a, ta, "double"), self.conv(b, tb, "double")
+        if op in ("<", "<=", ">", ">=", "==", "!="):
+            return f"(({a}) {op} ({b}))", "int"
+        if op == "%":
+            raise LowerError("'%' requires integer operands")
+        sfx = "f" if self.f32 else "d"
+        name = {"+": "add", "-": "sub", "*": "mul", "/": "div"}[op]
+        return f"__{sfx}{name}_rn({a}, {b})", "double"
+
+    def call(self, e: ks.Expr) -> str:
+        args = [self.conv(*self.ex(a), "double") for a in e.kids]
+        n = e.op
+        f = "f" if self.f32 else ""
+        if n == "sqrt":
+            return f"__{'f' if self.f32 else 'd'}sqrt_rn({args[0]})"
+        if n in LIBM1 and len(args) == 1:
+            return f"{n}{f}({args[0]})"
+        if n in LIBM2 and len(args) == 2:
+            return f"{n}{f}({args[0]}, {args[1]})"
+        raise LowerError(f"unknown function {n}/{len(args)}")
+
+    def load(self, e: ks.Expr) -> str:
+        self.n_loads += 1
+        offs = self.ref_offsets(e)
+        arr = f"ARR_{e.op}"
+        if offs is not None:
+            return f"m.template ld<{arr}, {', '.join(str(o) for o in offs)}>()"
+        self.n_dyn += 1
+        idx = ", ".join(self.conv(*self.ex(i), "int") for i in e.kids)
+        return f"m.template ldx<{arr}>({idx})"
+
+    # -- statements
+    def is_fma_temp(self, s: ks.Stmt) -> Optional[Tuple[ks.Expr, ks.Expr, ks.Expr]]:
+        if not (self.fma and s.lhs.kind == "var" and s.lhs.op.startswith("_v")):
+            return None
+        r = s.rhs
+        if r.kind == "bin" and r.op == "+" and r.kids[1].kind == "bin" and r.kids[1].op == "*":
+            a, (b, c) = r.kids[0], r.kids[1].kids
+            atoms = ("var", "int", "float")
+
+            def atom(x):
+                return x.kind in atoms or (x.kind == "un" and x.op == "-" and x.kids[0].kind in atoms)
+            if atom(a) and atom(b) and atom(c) and self.types.get(s.lhs.op) == "double":
+                return a, b, c
+        return None
+
+    def st(self, s: ks.Stmt, ind: int, out: List[str]):
+        pad = "    " * ind
+        k = s.kind
+        if k == "decl":
+            for name, dims, init in s.names:
+                if dims:
+                    raise LowerError("local arrays are not supported on the device path")
+                self.types[name] = s.ty
+                ty = "int" if s.ty == "int" else self.real()
+                if init is not None:
+                    c = self.conv(*self.ex(init), s.ty)
+                    out.append(f"{pad}{ty} {name} = {c};")
+                else:
+                    out.append(f"{pad}{ty} {name};")
+            return
+        if k == "assign":
+            fm = self.is_fma_temp(s)
+            if s.lhs.kind == "var":
+                name = s.lhs.op
+                if name not in self.types:
+                    raise LowerError(f"assignment to undeclared {name}")
+                tgt = self.types[name]
+                if fm:
+                    a, b, c = (self.conv(*self.ex(x), "double") for x in fm)
+                    self.n_fma += 1
+                    fn = "__fmaf_rn" if self.f32 else "__fma_rn"
+                    out.append(f"{pad}{name} = {fn}({b}, {c}, {a});")
+                    return
+                code, t = self.ex(s.rhs)
+                out.append(f"{pad}{name} = {self.conv(code, t, tgt)};")
+                # int temps defined once by an affine expression resolve subscripts statically
+                if tgt == "int" and self.assign_count.get(name, 0) == 1 and name not in self.loop_vars:
+                    a = self.as_affine(s.rhs)
+                    if a is not None:
+                        self.affine[name] = a
+                return
+            if s.lhs.kind == "ref":
+                arr = s.lhs.op
+                self.stored.add(arr)
+                want = "int" if self.arrays[arr].ty == "int" else "double"
+                code, t = self.ex(s.rhs)
+                val = self.conv(code, t, want)
+                offs = self.ref_offsets(s.lhs)
+                if offs is not None:
+                    out.append(f"{pad}m.template st<ARR_{arr}, {', '.join(map(str, offs))}>({val});")
+                else:
+                    idx = ", ".join(self.conv(*self.ex(i), "int") for i in s.lhs.kids)
+                    out.append(f"{pad}m.template stx<ARR_{arr}>({idx}, {val});")
+                return
+            raise LowerError("bad assignment target")
+        if k == "if":
+            c, _ = self.ex(s.cond)
+            out.append(f"{pad}if ({c}) {{")
+            self.st(s.then_s, ind + 1, out)
+            if s.else_s is not None:
+                out.append(f"{pad}}} else {{")
+                self.st(s.else_s, ind + 1, out)
+            out.append(f"{pad}}}")
+            return
+        if k == "block":
+            out.append(f"{pad}{{")
+            for c in s.stmts:
+                self.st(c, ind + 1, out)
+            out.append(f"{pad}}}")
+            return
+        if k == "empty":
+            return
+        if k == "call":
+            out.append(f"{pad}(void){self.call(s.call)};")
+            return
+        if k == "for":
+            raise LowerError("sequential loops inside a region body are not supported yet")
+        raise LowerError(f"statement kind {k}")
+
+    def bound_expr(self, e: ks.Expr) -> str:
+        c, t = self.ex(e)
+        if t != "int":
+            raise LowerError("loop bounds must be int")
+        return c.replace("m.template", "<bad>")
+
+    def loop_bounds(self) -> List[Tuple[str, str]]:
+        out = []
+        for l in self.region.loops:
+            if l.init.kind != "assign" or l.cond is None or l.cond.kind != "bin":
+                raise LowerError("unsupported loop header")
+            step = l.step
+            if not (step.kind == "assign" and step.rhs.kind == "bin" and step.rhs.op == "+"
+                    and step.rhs.kids[1].kind == "int" and step.rhs.kids[1].text == "1"):
+                raise LowerError("only unit-step loops are supported")
+            lo = self.bound_expr(l.init.rhs)
+            op = l.cond.op
+            hi = self.bound_expr(l.cond.kids[1])
+            if l.cond.kids[0].kind != "var" or l.cond.kids[0].op != l.loop_var:
+                raise LowerError("loop condition must test the loop variable")
+            if op == "<=":
+                hi = f"({hi}) + 1"
+            elif op != "<":
+                raise LowerError("loop condition must be < or <=")
+            out.append((lo, hi))
+        return out
+
+    def run(self) -> Lowered:
+        body_stmt = self.region.anchor.body
+        self.count_assigns(body_stmt)
+        # function-level locals other than loop vars
+        pre: List[str] = []
+        for s in self.fn.body.stmts:
+            if s.kind == "decl":
+                for name, dims, init in s.names:
+                    if name in self.loop_vars:
+                        continue
+                    if dims:
+                        raise LowerError("local arrays are not supported")
+                    self.types[name] = s.ty
+                    ty = "int" if s.ty == "int" else self.real()
+                    pre.append(f"    {ty} {name};")
+            elif s.kind == "for":
+                if s is not self.region.loops[0]:
+                    raise LowerError("only one loop nest per function is supported")
+            elif s.kind != "empty":
+                raise LowerError("statements outside the loop nest are not supported")
+        bounds = self.loop_bounds()
+        out: List[str] = list(pre)
+        self.st(body_stmt, 1, out)
+        sig = {a: self.sig.get(a) for a in self.arrays}
+        return Lowered(self.fn.name, self.fn.params, self.loop_vars, bounds,
+                       {a: (s if s is not None else [-1] * len(self.arrays[a].dims)) for a, s in sig.items()},
+                       self.stored, "\n".join(out), self.n_fma, self.n_loads, self.n_dyn, self.offrange)
+
+
+def lower_text(text: str, function: str, fma: bool, f32: bool = False) -> Lowered:
+    mod = ks.parse(text)
+    for reg in ks.find_regions(mod):
+        if reg.function.name == function:
+            return _Lowerer(reg.function, reg, fma, f32).run()
+    raise LowerError(f"no region in function {function}")
+
+
+# ---------------------------------------------------------------------------
+# Header generation
+
+FORMS = [("original", None, False), ("cse", "cse", False), ("cse_bulk", "cse+bulk", False),
+         ("cse_sat", "cse+sat", True), ("accsat", "accsat", True)]
+
+
+def _scalar_struct(params, f32):
+    real = "float" if f32 else "double"
+    lines = ["struct Scalars {"]
+    for p in params:
+        if not p.dims:
+            lines.append(f"    {'int' if p.ty == 'int' else real} {p.name};")
+    lines.append("};")
+    return lines
+
+
+def gen_function(nest: str, function: str, f32: bool = False) -> Tuple[str, dict]:
+    ns = function + ("_f32" if f32 else "")
+    texts = {}
+    for form, variant, fma in FORMS:
+        path = (os.path.join(ROOT, "nests", f"{nest}.c") if variant is None
+                else os.path.join(ROOT, "tests", "golden", "emitted", f"{nest}.{variant}.c"))
+        texts[form] = (open(path).read(), fma)
+    lows = {form: lower_text(t, function, fma, f32) for form, (t, fma) in texts.items()}
+    base = lows["original"]
+    arrays = [p for p in base.params if p.dims]
+    # merge signatures across forms (all forms must agree on static position maps)
+    sig = {}
+    for a in arrays:
+        cands = [l.sig[a.name] for l in lows.values() if any(x != -1 for x in l.sig[a.name])]
+        sig[a.name] = cands[0] if cands else [-1] * len(a.dims)
+        for c in cands:
+            if c != sig[a.name]:
+                raise LowerError(f"{function}: forms disagree on the position map of {a.name}")
+    stored = set().union(*(l.stored for l in lows.values()))
+    L = []
+    L.append(f"struct {ns} {{")
+    L.extend(_scalar_struct(base.params, f32))
+    L.append("enum : int {")
+    for i, a in enumerate(arrays):
+        L.append(f"    ARR_{a.name} = {i},")
+    L.append(f"    NARR = {len(arrays)}")
+    L.append("};")
+    L.append(f"static constexpr int NLOOP = {len(base.loop_vars)};")
+    L.append(f"static constexpr int MAXDIM = 8;")
+    L.append("// per array, per subscript position: index of the loop variable it is")
+    L.append("// relative to (0 = outermost marked loop), or -1 = absolute constant")
+    rows = ", ".join("{" + ", ".join(str(x) for x in (sig[a.name] + [-1] * (8 - len(a.dims)))) + "}"
+                     for a in arrays)
+    L.append(f"static __host__ __device__ constexpr int sig(int a, int p) {{ constexpr int t[NARR][8] = {{{rows}}}; return t[a][p]; }}")
+    L.append("static __host__ __device__ constexpr int ndim(int a) { constexpr int t[NARR] = {"
+             + ", ".join(str(len(a.dims)) for a in arrays) + "}; return t[a]; }")
+    L.append("// arrays never stored by any form: safe for the read-only (ld.global.nc) path")
+    L.append("static __host__ __device__ constexpr bool readonly(int a) { constexpr bool t[NARR] = {"
+             + ", ".join("false" if a.name in stored else "true" for a in arrays) + "}; return t[a]; }")
+    L.append("static __host__ __device__ constexpr bool is_int(int a) { constexpr bool t[NARR] = {"
+             + ", ".join("true" if a.ty == "int" else "false" for a in arrays) + "}; return t[a]; }")
+    L.append("static constexpr const char* array_names[NARR] = {" + ", ".join(f'"{a.name}"' for a in arrays) + "};")
+    sc = [p for p in base.params if not p.dims]
+    L.append(f"static constexpr int NSCALAR = {len(sc)};")
+    L.append("static constexpr const char* scalar_names[NSCALAR] = {" + ", ".join(f'"{p.name}"' for p in sc) + "};")
+    L.append("static constexpr bool scalar_is_int[NSCALAR] = {" + ", ".join("true" if p.ty == "int" else "false" for p in sc) + "};")
+    L.append("static inline void set_scalar(Scalars& s, int idx, long long iv, double dv) {")
+    L.append("    switch (idx) {")
+    for i, p in enumerate(sc):
+        L.append(f"        case {i}: s.{p.name} = {'(int)iv' if p.ty == 'int' else ('(float)dv' if f32 else 'dv')}; break;")
+    L.append("    }")
+    L.append("}")
+    L.append("// iteration space: half-open [lo, hi) per marked loop, outermost first")
+    L.append("static __host__ __device__ inline void bounds(const Scalars& s, long long lo[NLOOP], long long hi[NLOOP]) {")
+    for p in sc:
+        L.append(f"    const auto {p.name} = s.{p.name}; (void){p.name};")
+    for d, (lo, hi) in enumerate(base.bounds):
+        L.append(f"    lo[{d}] = {lo}; hi[{d}] = {hi};")
+    L.append("}")
+    meta = {}
+    for form, low in lows.items():
+        lv = ", ".join(f"const int {v}" for v in low.loop_vars)
+        L.append(f"// form {form}: {low.n_loads} static loads ({low.n_dyn_loads} data-dependent), "
+                 f"{low.n_fma} single-rounding FMA")
+        L.append(f"template <class M>")
+        L.append(f"static __device__ __forceinline__ void body_{form}(M& m, const Scalars& s_, {lv}) {{")
+        for p in sc:
+            ty = "int" if p.ty == "int" else ("float" if f32 else "double")
+            L.append(f"    {ty} {p.name} = s_.{p.name}; (void){p.name};")
+        L.append(low.body)
+        L.append("}")
+        meta[form] = {"loads": low.n_loads, "dyn_loads": low.n_dyn_loads, "fma": low.n_fma}
+    forms = [f for f, _, _ in FORMS]
+    L.append("// per acs_variant (ORIGINAL, CSE, CSE_BULK, CSE_SAT, ACCSAT)")
+    L.append("static constexpr int static_loads[5] = {" + ", ".join(str(meta[f]["loads"]) for f in forms) + "};")
+    L.append("static constexpr int fma_count[5] = {" + ", ".join(str(meta[f]["fma"]) for f in forms) + "};")
+    # static offset range per array/position over every form (host-side bounds check)
+    rng = {}
+    for low in lows.values():
+        for a, r in low.offrange.items():
+            cur = rng.setdefault(a, [list(x) for x in r])
+            for p, (lo_, hi_) in enumerate(r):
+                cur[p][0] = min(cur[p][0], lo_)
+                cur[p][1] = max(cur[p][1], hi_)
+    rows_lo, rows_hi = [], []
+    for a in arrays:
+        r = rng.get(a.name, [[0, 0]] * len(a.dims))
+        rows_lo.append("{" + ", ".join(str(x[0]) for x in r + [[0, 0]] * (8 - len(r))) + "}")
+        rows_hi.append("{" + ", ".join(str(x[1]) for x in r + [[0, 0]] * (8 - len(r))) + "}")
+    L.append("// min / max static subscript offset per array and position (all forms)")
+    L.append("static constexpr int off_lo[NARR][8] = {" + ", ".join(rows_lo) + "};")
+    L.append("static constexpr int off_hi[NARR][8] = {" + ", ".join(rows_hi) + "};")
+    L.append("static constexpr bool has_dynamic_index = " + ("true" if any(m_["dyn_loads"] for m_ in meta.values()) else "false") + ";")
+    args = ", ".join(f"pt[{d}]" for d in range(len(base.loop_vars)))
+    L.append("template <int FORM, class M>")
+    L.append("static __device__ __forceinline__ void body(M& m, const Scalars& s, const int* pt) {")
+    for fi, f in enumerate(forms):
+        kw = "if" if fi == 0 else "else if"
+        L.append(f"    {kw} constexpr (FORM == {fi}) body_{f}(m, s, {args});")
+    L.append("}")
+    L.append(f"}};  // struct {ns}")
+    return "\n".join(L) + "\n", meta
+
+
+NEST_FUNCS = {
+    "jacobi7": ["jacobi7"],
+    "swim": ["calc1", "calc2", "calc3"],
+    "clover": ["ideal_gas", "pdv_predict", "advec_cell_x"],
+    "wave4": ["wave4"],
+    "d3q19": ["stream_collide"],
+}
+
+
+def generate_all(out_dir: str) -> dict:
+    os.makedirs(out_dir, exist_ok=True)
+    allmeta = {}
+    for nest, fns in NEST_FUNCS.items():
+        parts = ["// GENERATED by paper_2306_13002_b200/lowering.py from nests/" + nest +
+                 ".c (original form) and tests/golden/emitted/" + nest + ".<variant>.c",
+                 "// (reference-emitted forms).  Do not edit: re-run `python -m "
+                 "paper_2306_13002_b200.lowering`.",
+                 "#pragma once", "namespace acs { namespace gen {"]
+        for fn in fns:
+            txt, meta = gen_function(nest, fn)
+            parts.append(txt)
+            allmeta[fn] = meta
+            if nest == "wave4":
+                txt, meta = gen_function(nest, fn, f32=True)
+                parts.append(txt)
+                allmeta[fn + "_f32"] = meta
+        parts.append("}}  // namespace acs::gen")
+        with open(os.path.join(out_dir, f"{nest}.cuh"), "w") as f:
+            f.write("\n".join(parts) + "\n")
+    return allmeta
+
+
+if __name__ == "__main__":
+    import json
+    meta = generate_all(os.path.join(ROOT, "paper_2306_13002_b200", "csrc", "gen"))
+    print(json.dumps(meta, indent=1))

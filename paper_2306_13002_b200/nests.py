@@ -186,7 +186,8 @@ def workload(kernel_id: str, size=None, dtype: str = "f64") -> Workload:
         d = (nz + 2, ny + 2, nx + 2)
         dims = {"src": d + (19,), "dst": d + (19,), "flags": d}
         sc = {"omega": 1.95, "zbeg": 1, "zend": nz + 1, "ny": d[1], "nx": d[2]}
-        fills = {"src": Fill("d3q19"), "dst": Fill("d3q19"), "flags": Fill("mask", p=0.1)}
+        fills = {"src": Fill("d3q19", -0.01, 0.01), "dst": Fill("d3q19", -0.01, 0.01),
+                 "flags": Fill("mask", p=0.1)}
         # 19 reads + 19 writes of 8 B + the 1-byte flag (uint8 on the device)
         return Workload(s, dims, sc, fills, "f64", nz * ny * nx, 19 * 8 * 2 + 1,
                         ["src", "flags"], ["dst"])
@@ -260,7 +261,7 @@ def make_inputs(w: Workload) -> Dict[str, np.ndarray]:
         elif fl.kind == "mask":
             a = (uniform(seed, n, 0.0, 1.0) < fl.p).astype(np.int32)
         elif fl.kind == "d3q19":
-            a = (np.tile(D3Q19_W, n // 19) * (1.0 + uniform(seed, n, -0.01, 0.01))).astype(fdt)
+            a = (np.tile(D3Q19_W, n // 19) * (1.0 + uniform(seed, n, fl.lo, fl.hi))).astype(fdt)
         elif fl.kind == "copy":
             a = out[fl.src].reshape(-1).copy()
         else:
@@ -273,3 +274,26 @@ def make_inputs(w: Workload) -> Dict[str, np.ndarray]:
 
 def scalar_values(w: Workload) -> Dict[str, float]:
     return dict(w.scalars)
+
+
+def device_inputs(w: Workload, native: bool = True, kernel=None, stream=None):
+    """Allocates and fills the workload directly in HBM (acs_fill: the same
+    SplitMix64 stream as make_inputs, so values are bit-identical).  Arrays
+    use the backend's preferred strides when `native`."""
+    import torch
+    from . import backend
+    k = kernel or backend.Kernel.lookup(w.spec.kernel_id)
+    tdt = torch.float32 if w.dtype == "f32" else torch.float64
+    out = {}
+    for p in w.spec.arrays:
+        dt = torch.int32 if p.ctype == "int" else tdt
+        dims = w.dims[p.name]
+        t = backend.empty_native(k, p.name, dims, dt) if native else torch.empty(dims, dtype=dt, device="cuda")
+        fl = w.fills[p.name]
+        if fl.kind == "copy":
+            backend.copy(t, out[fl.src], stream)
+        else:
+            lo = fl.value if fl.kind == "const" else fl.lo
+            backend.fill(t, fl.kind, SEED_BASE + p.position, lo, fl.hi, fl.p, stream)
+        out[p.name] = t
+    return out

@@ -1,0 +1,78 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/accsat_b200.h declares, and its registry agrees with the
+reference's own region keys and metrics (static load / FMA counts frozen in
+tests/golden/emitted/*.json, satcc-metrics-v1)."""
+import ctypes
+import glob
+import json
+import os
+import re
+
+import pytest
+
+from paper_2306_13002_b200 import backend, nests
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    out = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        txt = open(h).read()
+        out.update(re.findall(r"^\s*[\w\s\*]*?\b(acs_\w+)\s*\(", txt, re.M))
+    return out
+
+
+def test_library_exports_every_declared_symbol():
+    L = ctypes.CDLL(backend.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 12
+    for s in syms:
+        assert hasattr(L, s), f"{s} declared in include/ but not exported"
+
+
+def test_abi_version():
+    assert backend.lib().acs_abi_version() == 1
+
+
+def test_registry_matches_find_regions_keys():
+    assert sorted(backend.kernel_ids()) == sorted(nests.KERNELS)
+
+
+@pytest.mark.parametrize("kid", sorted(nests.KERNELS))
+def test_registry_metrics_match_reference_goldens(kid):
+    spec = nests.kernel(kid)
+    k = backend.Kernel.lookup(kid)
+    assert k.info["function"] == spec.function and k.info["region"] == spec.region
+    assert k.info["arrays"] == [a.name for a in spec.arrays]
+    assert k.info["scalars"] == [s.name for s in spec.scalars]
+    order = ["original", "cse", "cse+bulk", "cse+sat", "accsat"]
+    for vi, v in enumerate(order[1:], start=1):
+        with open(os.path.join(nests.GOLDEN_DIR, f"{spec.nest}.{v}.json")) as f:
+            reg = json.load(f)["regions"][spec.region]
+        assert reg["function"] == spec.function
+        assert k.info["static_loads"][0] == reg["static_loads_before"]
+        assert k.info["static_loads"][vi] == reg["static_loads_after"], (v, k.info["static_loads"])
+        assert k.info["fma_count"][vi] == reg["fma_count"], (v, k.info["fma_count"])
+
+
+def test_lookup_unknown_kernel_is_an_error():
+    with pytest.raises(backend.EvalError):
+        backend.Kernel.lookup("missing.c:nothing:0")
+
+
+def test_native_strides_d3q19_soa():
+    k = backend.Kernel.lookup("d3q19.c:stream_collide:0")
+    assert k.native_strides("src", (4, 5, 6, 19)) == (30, 6, 1, 120)
+    assert k.native_strides("flags", (4, 5, 6)) == (30, 6, 1)
+    j = backend.Kernel.lookup("jacobi7.c:jacobi7:0")
+    assert j.native_strides("A0", (4, 5, 6)) == (30, 6, 1)
+
+
+def test_launch_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    env = backend.Environment({}, {})
+    with pytest.raises(backend.InternalError):
+        backend.eval_region("jacobi7.c:jacobi7:0", env)

@@ -1,0 +1,203 @@
+"""GPU parity: every registered nest x variant x skeleton, through the C ABI,
+against the CPU oracle on the same seeded inputs.
+
+* ORIGINAL / CSE / CSE_BULK forms: BIT-EXACT against the compiled reference
+  text (gcc -ffp-contract=off), which tests/test_oracle.py pins bit-exact to
+  the reference interpreter.
+* CSE_SAT / ACCSAT forms compute each extracted FMA with ONE rounding on the
+  GPU, so they are compared BIT-EXACT against the FMA-rewritten reference text
+  (oracle ``*_fma``), and — against the two-rounding reference interpreter
+  itself — within the reference comparator's rule |d| <= 1e-12*max(|a|,|b|)
+  or |d| <= 1e-12 (proj/src/oracle.cpp:12, :30-38) for fp64.
+* wave4 fp32: bit-exact against the fp32 textual copy (fmaf-rewritten for the
+  saturated forms); vs the fp64 text within 1e-5 with a norm-wise floor
+  1e-5*max|ref|.
+"""
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+import cpu as oracle_cpu
+from paper_2306_13002_b200 import backend, nests
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = ["original", "cse", "cse+bulk", "cse+sat", "accsat"]
+SAT = {"cse+sat", "accsat"}
+
+# (kernel nest, sizes) — ragged and odd extents on purpose
+SIZES = {
+    "jacobi7": [8, (5, 6, 9), (33, 47, 70)],
+    "wave4": [6, (5, 4, 7), (19, 22, 61)],
+    "d3q19": [5, (3, 4, 6), (13, 17, 35)],
+    "swim": [12, (9, 14), (131, 257)],
+    "clover": [12, (7, 13), (131, 257)],
+}
+
+
+def _torch():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def to_device(k, name, a, native=True):
+    torch = _torch()
+    t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    if not native:
+        return t
+    st = k.native_strides(name, tuple(a.shape))
+    if st == tuple(t.stride()):
+        return t
+    d = torch.empty_strided(tuple(a.shape), st, dtype=t.dtype, device="cuda")
+    backend.copy(d, t)
+    return d
+
+
+def to_host(t):
+    torch = _torch()
+    if not t.is_contiguous():
+        rm = torch.empty(t.shape, dtype=t.dtype, device="cuda")
+        backend.copy(rm, t)
+        t = rm
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def run_gpu(kid, ins, scalars, variant, schedule, native=True):
+    k = backend.Kernel.lookup(kid)
+    dev = {n: to_device(k, n, a, native) for n, a in ins.items()}
+    k.launch(dev, scalars, variant, schedule)
+    return {n: to_host(t) for n, t in dev.items()}
+
+
+def bitwise_equal(a, b):
+    if a.dtype.kind == "f":
+        u = np.uint64 if a.itemsize == 8 else np.uint32
+        return np.array_equal(a.view(u), b.astype(a.dtype).view(u))
+    return np.array_equal(a, b)
+
+
+def cases():
+    out = []
+    for kid, spec in nests.KERNELS.items():
+        for size in SIZES[spec.nest]:
+            out.append((kid, size))
+    return out
+
+
+def schedules(kid):
+    k = backend.Kernel.lookup(kid)
+    return ["naive", "tiled"] if k.info["has_tiled"] else ["naive"]
+
+
+@pytest.mark.parametrize("kid,size", cases(), ids=[f"{k.split(':')[1]}-{s}" for k, s in cases()])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_parity_bitexact_vs_oracle(kid, size, variant):
+    spec = nests.kernel(kid)
+    w = nests.workload(kid, size)
+    ins = nests.make_inputs(w)
+    want = {n: a.copy() for n, a in ins.items()}
+    oracle_cpu.run(spec, want, w.scalars, variant, fma=variant in SAT)
+    for sched in schedules(kid):
+        got = run_gpu(kid, ins, w.scalars, variant, sched)
+        for n in w.write_arrays:
+            assert bitwise_equal(got[n], want[n]), \
+                f"{kid} {variant}/{sched} size={size}: '{n}' differs from the oracle " \
+                f"(max abs {np.max(np.abs(got[n] - want[n]))})"
+        for n in w.read_arrays:
+            if n not in w.write_arrays:
+                assert bitwise_equal(got[n], ins[n]), f"{kid}: read-only array '{n}' was modified"
+
+
+@pytest.mark.parametrize("size", [6, (19, 22, 61)])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_wave4_fp32_parity(size, variant):
+    kid = "wave4.c:wave4:0"
+    spec = nests.kernel(kid)
+    w = nests.workload(kid, size, dtype="f32")
+    ins = nests.make_inputs(w)
+    want = {n: a.copy() for n, a in ins.items()}
+    oracle_cpu.run(spec, want, w.scalars, variant, fma=variant in SAT, f32=True)
+    for sched in schedules(kid):
+        got = run_gpu(kid, ins, w.scalars, variant, sched)
+        assert bitwise_equal(got["un"], want["un"]), f"wave4 fp32 {variant}/{sched} differs"
+    # against the fp64 text: rel 1e-5 with a norm-wise floor
+    w64 = nests.workload(kid, size)
+    ins64 = {n: a.astype(np.float64) for n, a in ins.items()}
+    ref = {n: a.copy() for n, a in ins64.items()}
+    oracle_cpu.run(spec, ref, w64.scalars, "original")
+    d = np.abs(got["un"].astype(np.float64) - ref["un"])
+    floor = 1e-5 * np.max(np.abs(ref["un"]))
+    assert np.all((d <= 1e-5 * np.maximum(np.abs(ref["un"]), np.abs(got["un"]))) | (d <= floor))
+
+
+VEC = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "vectors", "*.npz")))
+
+
+@pytest.mark.parametrize("path", VEC, ids=[os.path.basename(p)[:-4] for p in VEC])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_gpu_vs_reference_interpreter(path, variant):
+    """Directly against the reference's own executor (golden vectors)."""
+    z = np.load(path)
+    fn = os.path.basename(path).split(".")[0]
+    spec = nests.kernel(fn)
+    scalars = json.loads(bytes(z["scalars"]).decode())
+    ins = {k[3:]: (z[k].astype(np.int32) if z[k].dtype.kind == "i" else z[k]) for k in z.files if k.startswith("in_")}
+    got = run_gpu(spec.kernel_id, ins, scalars, variant, "default")
+    for key in z.files:
+        if not key.startswith(f"out_{variant}_"):
+            continue
+        name = key[len(f"out_{variant}_"):]
+        want = z[key]
+        if variant in SAT:
+            d = np.abs(got[name] - want)
+            mag = np.maximum(np.abs(got[name]), np.abs(want))
+            assert np.all((d <= 1e-12 * mag) | (d <= 1e-12)), f"{fn}/{variant}/{name}"
+        else:
+            assert bitwise_equal(got[name], want), f"{fn}/{variant}/{name} differs from the reference interpreter"
+
+
+def test_rowmajor_and_native_layouts_agree():
+    kid = "d3q19.c:stream_collide:0"
+    w = nests.workload(kid, (7, 9, 12))
+    ins = nests.make_inputs(w)
+    a = run_gpu(kid, ins, w.scalars, "accsat", "default", native=True)
+    b = run_gpu(kid, ins, w.scalars, "accsat", "default", native=False)
+    assert bitwise_equal(a["dst"], b["dst"])
+
+
+def test_device_fill_matches_host_inputs():
+    torch = _torch()
+    for kid in ("d3q19.c:stream_collide:0", "clover.c:pdv_predict:1", "wave4.c:wave4:0"):
+        for dt in (("f64", "f32") if "wave4" in kid else ("f64",)):
+            w = nests.workload(kid, (5, 6, 7) if "clover" not in kid else (9, 11), dtype=dt)
+            ins = nests.make_inputs(w)
+            k = backend.Kernel.lookup(kid)
+            for p in w.spec.arrays:
+                fl = w.fills[p.name]
+                if fl.kind == "copy":
+                    continue
+                tdt = {np.float64: torch.float64, np.float32: torch.float32, np.int32: torch.int32}[ins[p.name].dtype.type]
+                t = backend.empty_native(k, p.name, ins[p.name].shape, tdt)
+                lo = fl.value if fl.kind == "const" else fl.lo
+                backend.fill(t, fl.kind, nests.SEED_BASE + p.position, lo, fl.hi, fl.p)
+                assert bitwise_equal(to_host(t), ins[p.name]), f"{kid}:{p.name}"
+
+
+def test_errors_are_loud():
+    kid = "jacobi7.c:jacobi7:0"
+    w = nests.workload(kid, 6)
+    ins = nests.make_inputs(w)
+    k = backend.Kernel.lookup(kid)
+    dev = {n: to_device(k, n, a) for n, a in ins.items()}
+    bad = dict(w.scalars, kend=w.scalars["kend"] + 1)   # would read A0[k+1] past the end
+    with pytest.raises(backend.EvalError):
+        k.launch(dev, bad, "accsat")
+    with pytest.raises(backend.EvalError):
+        k.launch({"A0": dev["A0"]}, w.scalars, "accsat")
+    with pytest.raises(backend.EvalError):
+        backend.Kernel.lookup("nope.c:f:0")
