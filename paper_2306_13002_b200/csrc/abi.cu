@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "registry.hpp"
+#include "tma.cuh"
 
 namespace acs {
 
@@ -36,6 +37,18 @@ void init_registry() {
 }  // namespace
 
 void set_error(const std::string& msg) { g_err = msg; }
+
+EncodeTiledFn tma_encoder() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
 void register_entry(Entry* e) { registry().push_back(e); }
 Entry* find_entry(const std::string& id) {
     for (Entry* e : registry())
@@ -304,20 +317,21 @@ acs_status acs_native_strides(const acs_kernel* k, const char* array_name, int n
         set_error("acs_native_strides: bad argument");
         return ACS_E_ARG;
     }
+    // Row pitch of the innermost spatial subscript padded to 16 elements, so
+    // every row starts 64/128-byte aligned and the TMA can describe the array
+    // (global strides must be multiples of 16 bytes).
+    auto pad = [](int64_t n) { return (n + 15) / 16 * 16; };
+    bool comp = false;
+    for (size_t i = 0; i < e->arrays.size(); ++i)
+        if (e->arrays[i] == array_name) comp = e->component_last[i] != 0;
+    const bool soa = e->soa_last_dim && ndim >= 2 && comp;
+    const int inner = soa ? ndim - 2 : ndim - 1;
     int64_t st = 1;
-    for (int p = ndim - 1; p >= 0; --p) {
+    for (int p = inner; p >= 0; --p) {
         strides_out[p] = st;
-        st *= dims[p];
+        st *= (p == inner && ndim > 1) ? pad(dims[p]) : dims[p];
     }
-    if (e->soa_last_dim && ndim >= 2 && std::string(array_name) != "flags") {
-        // q-major SoA: the trailing (distribution) subscript becomes the slowest.
-        int64_t cell = 1;
-        for (int p = ndim - 2; p >= 0; --p) {
-            strides_out[p] = cell;
-            cell *= dims[p];
-        }
-        strides_out[ndim - 1] = cell;
-    }
+    if (soa) strides_out[ndim - 1] = st;   // q-major SoA: the distribution subscript is slowest
     return ACS_OK;
 }
 

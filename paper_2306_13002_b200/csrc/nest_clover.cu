@@ -1,5 +1,6 @@
 // Registration of the clover nest functions (generated bodies: gen/clover.cuh).
 #include "registry.hpp"
+#include "kernels/march.cuh"
 #include "gen/clover.cuh"
 
 namespace acs {
@@ -11,6 +12,7 @@ void register_clover() {
         e.function = "ideal_gas";
         describe<gen::ideal_gas>(e, "clover.c", 0);
         fill_naive<gen::ideal_gas, double>(e, 0);
+        fill_march<gen::ideal_gas, double, 0, 128, 1, 3>(e, 0);
         register_entry(&e);
     }
     {
@@ -19,6 +21,7 @@ void register_clover() {
         e.function = "pdv_predict";
         describe<gen::pdv_predict>(e, "clover.c", 1);
         fill_naive<gen::pdv_predict, double>(e, 0);
+        fill_march<gen::pdv_predict, double, 0, 128, 1, 3>(e, 0);
         register_entry(&e);
     }
     {
@@ -27,6 +30,7 @@ void register_clover() {
         e.function = "advec_cell_x";
         describe<gen::advec_cell_x>(e, "clover.c", 2);
         fill_naive<gen::advec_cell_x, double>(e, 0);
+        fill_march<gen::advec_cell_x, double, 0, 128, 1, 3>(e, 0);
         register_entry(&e);
     }
 }

@@ -1,5 +1,6 @@
 // Registration of the d3q19 nest functions (generated bodies: gen/d3q19.cuh).
 #include "registry.hpp"
+#include "kernels/march.cuh"
 #include "gen/d3q19.cuh"
 
 namespace acs {
@@ -11,6 +12,7 @@ void register_d3q19() {
         e.function = "stream_collide";
         describe<gen::stream_collide>(e, "d3q19.c", 0);
         fill_naive<gen::stream_collide, double>(e, 0);
+        fill_march<gen::stream_collide, double, 1, 64, 4, 1>(e, 0);
         e.soa_last_dim = true;
         register_entry(&e);
     }

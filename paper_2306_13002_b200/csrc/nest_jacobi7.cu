@@ -1,5 +1,6 @@
 // Registration of the jacobi7 nest functions (generated bodies: gen/jacobi7.cuh).
 #include "registry.hpp"
+#include "kernels/march.cuh"
 #include "gen/jacobi7.cuh"
 
 namespace acs {
@@ -11,6 +12,7 @@ void register_jacobi7() {
         e.function = "jacobi7";
         describe<gen::jacobi7>(e, "jacobi7.c", 0);
         fill_naive<gen::jacobi7, double>(e, 0);
+        fill_march<gen::jacobi7, double, 0, 64, 4, 3>(e, 0);
         register_entry(&e);
     }
 }

@@ -1,5 +1,6 @@
 // Registration of the swim nest functions (generated bodies: gen/swim.cuh).
 #include "registry.hpp"
+#include "kernels/march.cuh"
 #include "gen/swim.cuh"
 
 namespace acs {
@@ -11,6 +12,7 @@ void register_swim() {
         e.function = "calc1";
         describe<gen::calc1>(e, "swim.c", 0);
         fill_naive<gen::calc1, double>(e, 0);
+        fill_march<gen::calc1, double, 0, 128, 1, 3>(e, 0);
         register_entry(&e);
     }
     {
@@ -19,6 +21,7 @@ void register_swim() {
         e.function = "calc2";
         describe<gen::calc2>(e, "swim.c", 1);
         fill_naive<gen::calc2, double>(e, 0);
+        fill_march<gen::calc2, double, 0, 128, 1, 3>(e, 0);
         register_entry(&e);
     }
     {
@@ -27,6 +30,7 @@ void register_swim() {
         e.function = "calc3";
         describe<gen::calc3>(e, "swim.c", 2);
         fill_naive<gen::calc3, double>(e, 0);
+        fill_march<gen::calc3, double, 0, 128, 1, 3>(e, 0);
         register_entry(&e);
     }
 }

@@ -1,5 +1,6 @@
 // Registration of the wave4 nest functions (generated bodies: gen/wave4.cuh).
 #include "registry.hpp"
+#include "kernels/march.cuh"
 #include "gen/wave4.cuh"
 
 namespace acs {
@@ -11,7 +12,9 @@ void register_wave4() {
         e.function = "wave4";
         describe<gen::wave4>(e, "wave4.c", 0);
         fill_naive<gen::wave4, double>(e, 0);
+        fill_march<gen::wave4, double, 0, 32, 8, 3>(e, 0);
         fill_naive<gen::wave4_f32, float>(e, 1);
+        fill_march<gen::wave4_f32, float, 0, 64, 8, 3>(e, 1);
         register_entry(&e);
     }
 }

@@ -38,7 +38,8 @@ struct Entry {
     int static_loads[5] = {0, 0, 0, 0, 0};
     int fma_count[5] = {0, 0, 0, 0, 0};
     LaunchFn launch[2][5][2] = {};
-    bool soa_last_dim = false;   // backend layout: trailing subscript made slowest (D3Q19 q)
+    bool soa_last_dim = false;   // backend layout: trailing component subscript made slowest (D3Q19 q)
+    std::vector<int> component_last;  // per array: trailing subscript is an absolute component index
 };
 
 void register_entry(Entry* e);
@@ -176,7 +177,10 @@ template <class NS>
 void describe(Entry& e, const char* file, int region) {
     e.region = region;
     e.n_loops = NS::NLOOP;
-    for (int a = 0; a < NS::NARR; ++a) e.arrays.push_back(NS::array_names[a]);
+    for (int a = 0; a < NS::NARR; ++a) {
+        e.arrays.push_back(NS::array_names[a]);
+        e.component_last.push_back(NS::ndim(a) >= 2 && NS::sig(a, NS::ndim(a) - 1) == -1 ? 1 : 0);
+    }
     for (int s = 0; s < NS::NSCALAR; ++s) {
         e.scalars.push_back(NS::scalar_names[s]);
         e.scalar_is_int.push_back(NS::scalar_is_int[s] ? 1 : 0);

@@ -65,6 +65,10 @@ class Lowered:
     n_loads: int = 0
     n_dyn_loads: int = 0
     offrange: Dict[str, List[List[int]]] = field(default_factory=dict)
+    ldrange: Dict[str, List[List[int]]] = field(default_factory=dict)
+    dynrange: Dict[str, list] = field(default_factory=dict)
+    dynsig: Dict[str, List[int]] = field(default_factory=dict)
+    loaded: set = field(default_factory=set)
 
 
 class LowerError(Exception):
@@ -93,6 +97,11 @@ class _Lowerer:
         self.assign_count: Dict[str, int] = {}
         self.sig: Dict[str, List[Optional[int]]] = {}
         self.offrange: Dict[str, List[List[int]]] = {}
+        self.ldrange: Dict[str, List[List[int]]] = {}     # static LOADS only
+        self.dynrange: Dict[str, List[Optional[List[int]]]] = {}  # value-set hints of ldx
+        self.dynsig: Dict[str, List[int]] = {}
+        self.int_assigns: Dict[str, List[ks.Expr]] = {}
+        self.loaded = set()
         self.stored = set()
         self.n_fma = self.n_loads = self.n_dyn = 0
 
@@ -124,6 +133,7 @@ class _Lowerer:
     def count_assigns(self, s: ks.Stmt):
         if s.kind == "assign" and s.lhs.kind == "var":
             self.assign_count[s.lhs.op] = self.assign_count.get(s.lhs.op, 0) + 1
+            self.int_assigns.setdefault(s.lhs.op, []).append(s.rhs)
         for c in ks.children(s):
             self.count_assigns(c)
 
@@ -226,12 +236,75 @@ class _Lowerer:
             return f"{n}{f}({args[0]}, {args[1]})"
         raise LowerError(f"unknown function {n}/{len(args)}")
 
+    def value_set(self, e: ks.Expr, seen=None) -> List[Optional[Affine]]:
+        """Possible affine values of an int subscript expression (None = not
+        affine in the loop variables).  Used only as a HINT for which box of a
+        dynamically indexed array a tile should stage; the kernels re-check
+        every dynamic index at run time."""
+        seen = set() if seen is None else seen
+        a = self.as_affine(e)
+        if a is not None:
+            return [a]
+        if e.kind == "var" and e.op in self.int_assigns and e.op not in seen:
+            seen = seen | {e.op}
+            out: List[Optional[Affine]] = []
+            for rhs in self.int_assigns[e.op]:
+                out.extend(self.value_set(rhs, seen))
+            return out
+        if e.kind == "bin" and e.op in ("+", "-"):
+            ls, rs = self.value_set(e.kids[0], seen), self.value_set(e.kids[1], seen)
+            out = []
+            for x in ls:
+                for y in rs:
+                    if x is None or y is None:
+                        out.append(None)
+                    elif e.op == "+" and (x.var is None or y.var is None):
+                        out.append(Affine(x.var or y.var, x.off + y.off))
+                    elif e.op == "-" and y.var is None:
+                        out.append(Affine(x.var, x.off - y.off))
+                    else:
+                        out.append(None)
+            return out
+        return [None]
+
+    def record_dynamic(self, e: ks.Expr):
+        arr = e.op
+        sig, rng = [], []
+        for idx in e.kids:
+            vals = [v for v in self.value_set(idx) if v is not None]
+            vars_ = {v.var for v in vals}
+            if not vals or len(vars_) != 1:
+                sig.append(-2)        # unknown: no staging for this position
+                rng.append(None)
+                continue
+            var = vars_.pop()
+            sig.append(self.loop_vars.index(var) if var is not None else -1)
+            rng.append([min(v.off for v in vals), max(v.off for v in vals)])
+        old = self.dynsig.get(arr)
+        if old is not None and old != sig:
+            sig = [a if a == b else -2 for a, b in zip(old, sig)]
+        self.dynsig[arr] = sig
+        cur = self.dynrange.setdefault(arr, [None] * len(rng))
+        for p, r in enumerate(rng):
+            if sig[p] == -2 or r is None:
+                cur[p] = None
+            elif cur[p] is None:
+                cur[p] = list(r)
+            else:
+                cur[p] = [min(cur[p][0], r[0]), max(cur[p][1], r[1])]
+
     def load(self, e: ks.Expr) -> str:
         self.n_loads += 1
+        self.loaded.add(e.op)
         offs = self.ref_offsets(e)
         arr = f"ARR_{e.op}"
         if offs is not None:
+            r = self.ldrange.setdefault(e.op, [[o, o] for o in offs])
+            for p, o in enumerate(offs):
+                r[p][0] = min(r[p][0], o)
+                r[p][1] = max(r[p][1], o)
             return f"m.template ld<{arr}, {', '.join(str(o) for o in offs)}>()"
+        self.record_dynamic(e)
         self.n_dyn += 1
         idx = ", ".join(self.conv(*self.ex(i), "int") for i in e.kids)
         return f"m.template ldx<{arr}>({idx})"
@@ -378,7 +451,8 @@ class _Lowerer:
         sig = {a: self.sig.get(a) for a in self.arrays}
         return Lowered(self.fn.name, self.fn.params, self.loop_vars, bounds,
                        {a: (s if s is not None else [-1] * len(self.arrays[a].dims)) for a, s in sig.items()},
-                       self.stored, "\n".join(out), self.n_fma, self.n_loads, self.n_dyn, self.offrange)
+                       self.stored, "\n".join(out), self.n_fma, self.n_loads, self.n_dyn, self.offrange,
+                       self.ldrange, self.dynrange, self.dynsig, self.loaded)
 
 
 def lower_text(text: str, function: str, fma: bool, f32: bool = False) -> Lowered:
@@ -498,6 +572,54 @@ def gen_function(nest: str, function: str, f32: bool = False) -> Tuple[str, dict
     L.append("// min / max static subscript offset per array and position (all forms)")
     L.append("static constexpr int off_lo[NARR][8] = {" + ", ".join(rows_lo) + "};")
     L.append("static constexpr int off_hi[NARR][8] = {" + ", ".join(rows_hi) + "};")
+    # staging tables: per array/position, the box of LOADED elements relative to the
+    # point (static loads + value-set hints of data-dependent loads)
+    stage = {}
+    for a in arrays:
+        nd = len(a.dims)
+        sg = list(sig[a.name])
+        lo_ = [None] * nd
+        hi_ = [None] * nd
+        ok = True
+        for low in lows.values():
+            if a.name in low.ldrange:
+                for p, (x, y) in enumerate(low.ldrange[a.name]):
+                    lo_[p] = x if lo_[p] is None else min(lo_[p], x)
+                    hi_[p] = y if hi_[p] is None else max(hi_[p], y)
+            if a.name in low.dynsig:
+                ds, dr = low.dynsig[a.name], low.dynrange[a.name]
+                for p in range(nd):
+                    if ds[p] == -2 or dr[p] is None:
+                        ok = False
+                        continue
+                    if all(v == -1 for v in sig[a.name]) and not any(a.name in l.ldrange for l in lows.values()):
+                        sg[p] = ds[p]
+                    elif ds[p] != sg[p]:
+                        ok = False
+                        continue
+                    lo_[p] = dr[p][0] if lo_[p] is None else min(lo_[p], dr[p][0])
+                    hi_[p] = dr[p][1] if hi_[p] is None else max(hi_[p], dr[p][1])
+        loaded = any(a.name in l.loaded for l in lows.values())
+        # an array written by the nest is never staged: a staged copy could be
+        # stale after the thread's own store (load-after-store, e.g. the
+        # original advec re-reads mass_flux_x)
+        stage[a.name] = (loaded and ok and a.name not in stored and all(v is not None for v in lo_), sg,
+                         [v if v is not None else 0 for v in lo_], [v if v is not None else 0 for v in hi_])
+    def row(vals):
+        return "{" + ", ".join(str(x) for x in list(vals) + [0] * (8 - len(vals))) + "}"
+    L.append("// staging (TMA) tables: loaded box per array/position relative to the point")
+    L.append("static __host__ __device__ constexpr bool stageable(int a) { constexpr bool t[NARR] = {"
+             + ", ".join("true" if stage[a.name][0] else "false" for a in arrays) + "}; return t[a]; }")
+    L.append("static __host__ __device__ constexpr bool is_loaded(int a) { constexpr bool t[NARR] = {"
+             + ", ".join("true" if any(a.name in l.loaded for l in lows.values()) else "false" for a in arrays)
+             + "}; return t[a]; }")
+    L.append("static __host__ __device__ constexpr int ld_sig(int a, int p) { constexpr int t[NARR][8] = {"
+             + ", ".join("{" + ", ".join(str(x) for x in stage[a.name][1] + [-1] * (8 - len(a.dims))) + "}" for a in arrays)
+             + "}; return t[a][p]; }")
+    L.append("static __host__ __device__ constexpr int ld_lo(int a, int p) { constexpr int t[NARR][8] = {"
+             + ", ".join(row(stage[a.name][2]) for a in arrays) + "}; return t[a][p]; }")
+    L.append("static __host__ __device__ constexpr int ld_hi(int a, int p) { constexpr int t[NARR][8] = {"
+             + ", ".join(row(stage[a.name][3]) for a in arrays) + "}; return t[a][p]; }")
     L.append("static constexpr bool has_dynamic_index = " + ("true" if any(m_["dyn_loads"] for m_ in meta.values()) else "false") + ";")
     args = ", ".join(f"pt[{d}]" for d in range(len(base.loop_vars)))
     L.append("template <int FORM, class M>")

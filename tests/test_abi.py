@@ -63,10 +63,13 @@ def test_lookup_unknown_kernel_is_an_error():
 
 def test_native_strides_d3q19_soa():
     k = backend.Kernel.lookup("d3q19.c:stream_collide:0")
-    assert k.native_strides("src", (4, 5, 6, 19)) == (30, 6, 1, 120)
-    assert k.native_strides("flags", (4, 5, 6)) == (30, 6, 1)
+    # q-major SoA, x pitch padded to 16 elements
+    assert k.native_strides("src", (4, 5, 6, 19)) == (80, 16, 1, 320)
+    assert k.native_strides("flags", (4, 5, 6)) == (80, 16, 1)
     j = backend.Kernel.lookup("jacobi7.c:jacobi7:0")
-    assert j.native_strides("A0", (4, 5, 6)) == (30, 6, 1)
+    assert j.native_strides("A0", (4, 5, 32)) == (160, 32, 1)
+    s = backend.Kernel.lookup("swim.c:calc1:0")
+    assert s.native_strides("u", (8193, 8193)) == (8208, 1)
 
 
 def test_launch_without_gpu_fails_loudly():
