@@ -63,10 +63,14 @@ typedef enum {
 
 /* Kernel skeleton: NAIVE = one thread per point, every array reference of the
  * form is its own global load in source order (what a directive compiler
- * makes of the text); TILED = the B200 skeleton (shared-memory plane tiles,
- * register queues along the sweep axis, vectorised streams).  DEFAULT picks
- * NAIVE for ORIGINAL and the best registered skeleton otherwise. */
+ * makes of the text); TILED = the B200 marching-tile skeleton (TMA boxes of
+ * every loaded array staged in a shared-memory ring ahead of compute).
+ * DEFAULT = NAIVE for ORIGINAL (faithful baseline) and the preferred slot
+ * (first tiled configuration, or the acs_tune winner) otherwise. */
 typedef enum { ACS_SCHED_DEFAULT = 0, ACS_SCHED_NAIVE = 1, ACS_SCHED_TILED = 2 } acs_schedule;
+/* ACS_SCHED_SLOT(i): an explicit registered configuration (slot 0 = naive,
+ * slots 1.. = tiled configurations, see acs_kernel_schedule_name). */
+#define ACS_SCHED_SLOT(i) ((acs_schedule)(16 + (i)))
 
 typedef struct {
     const char* name;              /* parameter name in the nest text */
@@ -97,6 +101,7 @@ typedef struct {
     int32_t fma_count[5];          /* per acs_variant: single-rounding FMAs per point */
     int32_t has_tiled;             /* a TILED skeleton is registered */
     int32_t has_f32;               /* an fp32 instantiation is registered */
+    int32_t n_schedules;           /* registered slots (naive + tiled configurations), fp64 */
 } acs_kernel_info;
 
 int acs_abi_version(void);
@@ -116,6 +121,19 @@ int acs_kernel_scalar_is_int(const acs_kernel* k, int index);
 acs_status acs_launch(const acs_kernel* k, acs_variant variant, acs_schedule schedule,
                       const acs_array* arrays, int n_arrays,
                       const acs_scalar* scalars, int n_scalars, void* cuda_stream);
+
+/* Name of schedule slot `slot` for precision 0 (fp64) / 1 (fp32); NULL if absent. */
+const char* acs_kernel_schedule_name(const acs_kernel* k, int precision, int slot);
+
+/* Autotuning: times every registered slot for this variant on these arrays
+ * (each `reps` launches after one warm-up; the arrays are updated as by
+ * repeated launches), records the fastest as what ACS_SCHED_DEFAULT /
+ * ACS_SCHED_TILED use for this (kernel, precision, variant) from now on, and
+ * returns it.  ms_per_launch[slot] (optional, kMaxSched=8 entries) receives
+ * the timings (negative = slot absent).  Synchronous. */
+acs_status acs_tune(const acs_kernel* k, acs_variant variant, const acs_array* arrays, int n_arrays,
+                    const acs_scalar* scalars, int n_scalars, void* cuda_stream, int reps, int* best_slot,
+                    float* ms_per_launch);
 
 /* Device data utilities (synthetic inputs, layout remaps). */
 typedef enum { ACS_FILL_UNIFORM = 0, ACS_FILL_CONST = 1, ACS_FILL_MASK = 2, ACS_FILL_D3Q19 = 3 } acs_fill_kind;

@@ -59,7 +59,7 @@ class AcsKernelInfo(ctypes.Structure):
     _fields_ = [("kernel_id", ctypes.c_char_p), ("function", ctypes.c_char_p), ("region", ctypes.c_int32),
                 ("n_loops", ctypes.c_int32), ("n_arrays", ctypes.c_int32), ("n_scalars", ctypes.c_int32),
                 ("static_loads", ctypes.c_int32 * 5), ("fma_count", ctypes.c_int32 * 5),
-                ("has_tiled", ctypes.c_int32), ("has_f32", ctypes.c_int32)]
+                ("has_tiled", ctypes.c_int32), ("has_f32", ctypes.c_int32), ("n_schedules", ctypes.c_int32)]
 
 
 EXPORTS = {
@@ -74,6 +74,10 @@ EXPORTS = {
     "acs_kernel_scalar_is_int": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "acs_launch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(AcsArray),
                                   ctypes.c_int, ctypes.POINTER(AcsScalar), ctypes.c_int, ctypes.c_void_p]),
+    "acs_kernel_schedule_name": (ctypes.c_char_p, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]),
+    "acs_tune": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(AcsArray), ctypes.c_int,
+                                ctypes.POINTER(AcsScalar), ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_float)]),
     "acs_fill": (ctypes.c_int, [ctypes.POINTER(AcsArray), ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
                                 ctypes.c_double, ctypes.c_double, ctypes.c_void_p]),
     "acs_copy": (ctypes.c_int, [ctypes.POINTER(AcsArray), ctypes.POINTER(AcsArray), ctypes.c_void_p]),
@@ -163,14 +167,16 @@ class Kernel:
         info = {"function": inf.function.decode(), "region": inf.region, "n_loops": inf.n_loops,
                 "static_loads": list(inf.static_loads), "fma_count": list(inf.fma_count),
                 "has_tiled": bool(inf.has_tiled), "has_f32": bool(inf.has_f32),
+                "n_schedules": inf.n_schedules,
+                "schedules": [[(lib().acs_kernel_schedule_name(h, prec, i) or b"").decode() for i in range(8)]
+                              for prec in (0, 1)],
                 "arrays": [lib().acs_kernel_array_name(h, i).decode() for i in range(inf.n_arrays)],
                 "scalars": [lib().acs_kernel_scalar_name(h, i).decode() for i in range(inf.n_scalars)],
                 "scalar_is_int": [lib().acs_kernel_scalar_is_int(h, i) for i in range(inf.n_scalars)]}
         return cls(kernel_id, h.value, info)
 
-    def launch(self, arrays: Dict[str, object], scalars: Dict[str, float], variant: str = "accsat",
-               schedule: str = "default", stream=None) -> None:
-        """Asynchronous launch on `stream` (torch stream; default current)."""
+    @staticmethod
+    def _pack(arrays, scalars):
         descs = (AcsArray * len(arrays))(*[describe(n, t) for n, t in arrays.items()])
         sc = (AcsScalar * len(scalars))()
         for i, (n, v) in enumerate(scalars.items()):
@@ -179,8 +185,27 @@ class Kernel:
             sc[i].is_int = 1 if is_int else 0
             sc[i].i = int(v) if is_int else 0
             sc[i].d = float(v)
-        _check(lib().acs_launch(self.handle, VARIANTS[variant], SCHEDULES[schedule], descs, len(arrays), sc,
+        return descs, sc
+
+    def launch(self, arrays: Dict[str, object], scalars: Dict[str, float], variant: str = "accsat",
+               schedule="default", stream=None) -> None:
+        """Asynchronous launch on `stream` (torch stream; default current).
+        `schedule`: "default" | "naive" | "tiled" | int slot (0 = naive)."""
+        descs, sc = self._pack(arrays, scalars)
+        sched = 16 + schedule if isinstance(schedule, int) else SCHEDULES[schedule]
+        _check(lib().acs_launch(self.handle, VARIANTS[variant], sched, descs, len(arrays), sc,
                                 len(scalars), _stream_handle(stream)), f"acs_launch({self.kernel_id}, {variant})")
+
+    def tune(self, arrays, scalars, variant: str = "accsat", reps: int = 3, stream=None):
+        """acs_tune: times every registered schedule slot on these arrays and
+        makes the fastest the default for this variant.  Returns
+        (best_slot, {slot: ms})."""
+        descs, sc = self._pack(arrays, scalars)
+        best = ctypes.c_int(-1)
+        ms = (ctypes.c_float * 8)()
+        _check(lib().acs_tune(self.handle, VARIANTS[variant], descs, len(arrays), sc, len(scalars),
+                              _stream_handle(stream), reps, ctypes.byref(best), ms), f"acs_tune({self.kernel_id})")
+        return best.value, {i: ms[i] for i in range(8) if ms[i] >= 0}
 
     def native_strides(self, name: str, dims: Tuple[int, ...]) -> Tuple[int, ...]:
         d = (ctypes.c_int64 * len(dims))(*dims)

@@ -154,6 +154,12 @@ bool make_desc(const acs_array* a, StridedDesc& d, long long& n) {
     return true;
 }
 
+int precision_of(const acs_array* arrays, int n) {
+    for (int i = 0; i < n; ++i)
+        if (arrays[i].dtype == ACS_F32) return 1;
+    return 0;
+}
+
 int grid_for(long long n) {
     long long g = (n + 255) / 256;
     const long long cap = 148LL * 16;  // persistent-ish: 16 CTAs per SM, grid-stride
@@ -212,8 +218,9 @@ acs_status acs_kernel_get_info(const acs_kernel* k, acs_kernel_info* out) {
         out->static_loads[v] = e->static_loads[v];
         out->fma_count[v] = e->fma_count[v];
     }
-    out->has_tiled = e->launch[0][ACS_ACCSAT][1] != nullptr;
+    out->has_tiled = e->n_sched[0] > 1;
     out->has_f32 = e->launch[1][0][0] != nullptr;
+    out->n_schedules = e->n_sched[0];
     return ACS_OK;
 }
 
@@ -244,23 +251,85 @@ acs_status acs_launch(const acs_kernel* k, acs_variant variant, acs_schedule sch
         set_error("acs_launch: unknown variant");
         return ACS_E_ARG;
     }
-    // precision from the first real-typed array argument
-    int prec = 0;
-    for (int i = 0; i < n_arrays; ++i)
-        if (arrays[i].dtype == ACS_F32) prec = 1;
-    int sched;
+    const int prec = precision_of(arrays, n_arrays);
+    int slot;
     if (schedule == ACS_SCHED_DEFAULT)
-        sched = (variant != ACS_ORIGINAL && e->launch[prec][variant][1]) ? 1 : 0;
+        slot = variant == ACS_ORIGINAL ? 0 : e->best[prec][variant];
+    else if (schedule == ACS_SCHED_NAIVE)
+        slot = 0;
+    else if (schedule == ACS_SCHED_TILED)
+        slot = e->best[prec][variant] > 0 ? e->best[prec][variant] : 1;
     else
-        sched = schedule == ACS_SCHED_TILED ? 1 : 0;
-    LaunchFn fn = e->launch[prec][variant][sched];
+        slot = (int)schedule - 16;
+    LaunchFn fn = (slot >= 0 && slot < kMaxSched) ? e->launch[prec][variant][slot] : nullptr;
     if (!fn) {
-        set_error(e->kernel_id + ": no " + (sched ? "tiled" : "naive") + " kernel for variant " +
+        set_error(e->kernel_id + ": no kernel in schedule slot " + std::to_string(slot) + " for variant " +
                   std::to_string(variant) + (prec ? " (fp32)" : ""));
         return ACS_E_NO_KERNEL;
     }
     LaunchReq r{arrays, n_arrays, scalars, n_scalars, static_cast<cudaStream_t>(cuda_stream)};
     return fn(r);
+}
+
+const char* acs_kernel_schedule_name(const acs_kernel* k, int precision, int slot) {
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    if (!e || precision < 0 || precision > 1 || slot < 0 || slot >= kMaxSched || !e->launch[precision][0][slot])
+        return nullptr;
+    return e->sched_name[precision][slot].c_str();
+}
+
+acs_status acs_tune(const acs_kernel* k, acs_variant variant, const acs_array* arrays, int n_arrays,
+                    const acs_scalar* scalars, int n_scalars, void* cuda_stream, int reps, int* best_slot,
+                    float* ms_per_launch) {
+    if (!k || (int)variant < 0 || (int)variant > 4 || reps < 1) {
+        set_error("acs_tune: bad argument");
+        return ACS_E_ARG;
+    }
+    Entry* e = const_cast<Entry*>(reinterpret_cast<const Entry*>(k));
+    const int prec = precision_of(arrays, n_arrays);
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    LaunchReq r{arrays, n_arrays, scalars, n_scalars, s};
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    int bslot = -1;
+    for (int slot = 0; slot < kMaxSched; ++slot) {
+        if (ms_per_launch) ms_per_launch[slot] = -1.0f;
+        LaunchFn fn = e->launch[prec][variant][slot];
+        if (!fn) continue;
+        acs_status st = fn(r);   // warm-up (and TMA attribute setup)
+        if (st != ACS_OK) {
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            return st;
+        }
+        cudaEventRecord(e0, s);
+        for (int i = 0; i < reps; ++i) fn(r);
+        cudaEventRecord(e1, s);
+        if (cudaEventSynchronize(e1) != cudaSuccess) {
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            return check_launch("acs_tune");
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ms /= reps;
+        if (ms_per_launch) ms_per_launch[slot] = ms;
+        if (ms < best) {
+            best = ms;
+            bslot = slot;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (bslot < 0) {
+        set_error("acs_tune: no registered schedule");
+        return ACS_E_NO_KERNEL;
+    }
+    e->best[prec][variant] = bslot;
+    if (best_slot) *best_slot = bslot;
+    return check_launch("acs_tune");
 }
 
 acs_status acs_fill(const acs_array* a, acs_fill_kind kind, uint64_t seed, double lo, double hi, double p,

@@ -271,9 +271,12 @@ __device__ __forceinline__ void march_issue(unsigned char* slot_base, const TmaM
     }
 }
 
-template <class NS, class T, int FORM, int LAYOUT, int TX, int TY, int PF>
-__global__ void __launch_bounds__(TX* TY) march_kernel(const __grid_constant__ KernelArgs<NS> args,
+// TX x TY points per tile, BX x BY threads: each thread computes (TX/BX) x (TY/BY)
+// points per march step, amortising the step's barrier / mbarrier wait.
+template <class NS, class T, int FORM, int LAYOUT, int TX, int TY, int BX, int BY, int PF>
+__global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ KernelArgs<NS> args,
                                                        const __grid_constant__ TmaMaps<NS> maps, int kchunk) {
+    static_assert(TX % BX == 0 && TY % BY == 0, "tile must be a multiple of the block");
     using P = MarchPlan<NS, T, LAYOUT, TX, TY>;
     using M = MarchMem<NS, T, LAYOUT, TX, TY, PF>;
     constexpr int D = M::D;
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(TX* TY) march_kernel(const __grid_constant__ K
     uint64_t* bars = reinterpret_cast<uint64_t*>(stat + P::static_bytes());   // D ring + 1 static
 
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int tid = ty * TX + tx;
+    const int tid = ty * BX + tx;
     const int orgx = args.lo[P::X] + blockIdx.x * TX;
     const int orgy = NS::NLOOP == 3 ? args.lo[1] + blockIdx.y * TY : 0;
     const int kb = args.lo[0] + blockIdx.z * kchunk;
@@ -313,11 +316,7 @@ __global__ void __launch_bounds__(TX* TY) march_kernel(const __grid_constant__ K
     // loop below waits only for the newest bundle of each step.
     for (int B = 0; B < MS - 1 && B < nb; ++B) mbar_wait(&bars[B % D], 0);
 
-    const int x = orgx + tx, y = orgy + ty;
-    const bool active = x < args.hi[P::X] && (NS::NLOOP < 3 || y < args.hi[1]);
     int pt[NS::NLOOP];
-    pt[P::X] = x;
-    if constexpr (NS::NLOOP == 3) pt[1] = y;
     M m{NaiveMem<NS, T, false>{args, pt}, ring, stat, 0, tx, ty, 0, orgx, orgy, {}};
 #pragma unroll
     for (int a = 0; a < NS::NARR; ++a) m.sh[a] = xshift<P, NS>(a, orgx);
@@ -335,11 +334,22 @@ __global__ void __launch_bounds__(TX* TY) march_kernel(const __grid_constant__ K
         }
         const int Bw = s + MS - 1;
         mbar_wait(&bars[Bw % D], (uint32_t)((Bw / D) & 1));
-        if (active) {
-            pt[0] = kb + s;
-            m.k = kb + s;
-            m.newest = Bw % D;
-            NS::template body<FORM>(m, args.s, pt);
+        pt[0] = kb + s;
+        m.k = kb + s;
+        m.newest = Bw % D;
+#pragma unroll
+        for (int ry = 0; ry < TY / BY; ++ry) {
+#pragma unroll
+            for (int rx = 0; rx < TX / BX; ++rx) {
+                m.lx = tx + rx * BX;
+                m.ly = ty + ry * BY;
+                const int x = orgx + m.lx, y = orgy + m.ly;
+                if (x < args.hi[P::X] && (NS::NLOOP < 3 || y < args.hi[1])) {
+                    pt[P::X] = x;
+                    if constexpr (NS::NLOOP == 3) pt[1] = y;
+                    NS::template body<FORM>(m, args.s, pt);
+                }
+            }
         }
     }
 }
@@ -419,7 +429,7 @@ bool encode_maps(const LaunchReq& r, TmaMaps<NS>& maps) {
     return true;
 }
 
-template <class NS, class T, int FORM, int LAYOUT, int TX, int TY, int PF>
+template <class NS, class T, int FORM, int LAYOUT, int TX, int TY, int BX, int BY, int PF>
 acs_status launch_march(const LaunchReq& r) {
     using P = MarchPlan<NS, T, LAYOUT, TX, TY>;
     static_assert(P::usable(), "march skeleton: nest not stageable");
@@ -436,7 +446,7 @@ acs_status launch_march(const LaunchReq& r) {
     }
     constexpr int D = P::maxspan() + PF;
     constexpr int smem = D * P::slot_bytes() + P::static_bytes() + (D + 1) * 8;
-    auto kern = march_kernel<NS, T, FORM, LAYOUT, TX, TY, PF>;
+    auto kern = march_kernel<NS, T, FORM, LAYOUT, TX, TY, BX, BY, PF>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -455,17 +465,22 @@ acs_status launch_march(const LaunchReq& r) {
     if (kchunk > nz) kchunk = nz;
     const long long chunks = (nz + kchunk - 1) / kchunk;
     dim3 grid((unsigned)((nx + TX - 1) / TX), (unsigned)(NL == 3 ? (ny + TY - 1) / TY : 1), (unsigned)chunks);
-    kern<<<grid, dim3(TX, TY, 1), smem, r.stream>>>(ka, maps, (int)kchunk);
+    kern<<<grid, dim3(BX, BY, 1), smem, r.stream>>>(ka, maps, (int)kchunk);
     return check_launch("march");
 }
 
-template <class NS, class T, int LAYOUT, int TX, int TY, int PF>
+template <class NS, class T, int LAYOUT, int TX, int TY, int BX, int BY, int PF>
 void fill_march(Entry& e, int prec) {
-    e.launch[prec][0][1] = &launch_march<NS, T, 0, LAYOUT, TX, TY, PF>;
-    e.launch[prec][1][1] = &launch_march<NS, T, 1, LAYOUT, TX, TY, PF>;
-    e.launch[prec][2][1] = &launch_march<NS, T, 2, LAYOUT, TX, TY, PF>;
-    e.launch[prec][3][1] = &launch_march<NS, T, 3, LAYOUT, TX, TY, PF>;
-    e.launch[prec][4][1] = &launch_march<NS, T, 4, LAYOUT, TX, TY, PF>;
+    const int slot = e.n_sched[prec]++;
+    e.launch[prec][0][slot] = &launch_march<NS, T, 0, LAYOUT, TX, TY, BX, BY, PF>;
+    e.launch[prec][1][slot] = &launch_march<NS, T, 1, LAYOUT, TX, TY, BX, BY, PF>;
+    e.launch[prec][2][slot] = &launch_march<NS, T, 2, LAYOUT, TX, TY, BX, BY, PF>;
+    e.launch[prec][3][slot] = &launch_march<NS, T, 3, LAYOUT, TX, TY, BX, BY, PF>;
+    e.launch[prec][4][slot] = &launch_march<NS, T, 4, LAYOUT, TX, TY, BX, BY, PF>;
+    e.sched_name[prec][slot] = "march tile " + std::to_string(TX) + "x" + std::to_string(TY) + " block " +
+                               std::to_string(BX) + "x" + std::to_string(BY) + " pf " + std::to_string(PF);
+    for (int v = 0; v < 5; ++v)
+        if (e.best[prec][v] == 0 && v != ACS_ORIGINAL) e.best[prec][v] = slot;
 }
 
 }  // namespace acs

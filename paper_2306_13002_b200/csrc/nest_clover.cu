@@ -12,7 +12,9 @@ void register_clover() {
         e.function = "ideal_gas";
         describe<gen::ideal_gas>(e, "clover.c", 0);
         fill_naive<gen::ideal_gas, double>(e, 0);
-        fill_march<gen::ideal_gas, double, 0, 128, 1, 3>(e, 0);
+        fill_march<gen::ideal_gas, double, 0, 128, 1, 128, 1, 3>(e, 0);
+        fill_march<gen::ideal_gas, double, 0, 128, 1, 64, 1, 3>(e, 0);
+        fill_march<gen::ideal_gas, double, 0, 64, 1, 64, 1, 4>(e, 0);
         register_entry(&e);
     }
     {
@@ -21,7 +23,9 @@ void register_clover() {
         e.function = "pdv_predict";
         describe<gen::pdv_predict>(e, "clover.c", 1);
         fill_naive<gen::pdv_predict, double>(e, 0);
-        fill_march<gen::pdv_predict, double, 0, 128, 1, 3>(e, 0);
+        fill_march<gen::pdv_predict, double, 0, 128, 1, 128, 1, 3>(e, 0);
+        fill_march<gen::pdv_predict, double, 0, 128, 1, 64, 1, 3>(e, 0);
+        fill_march<gen::pdv_predict, double, 0, 64, 1, 64, 1, 4>(e, 0);
         register_entry(&e);
     }
     {
@@ -30,7 +34,9 @@ void register_clover() {
         e.function = "advec_cell_x";
         describe<gen::advec_cell_x>(e, "clover.c", 2);
         fill_naive<gen::advec_cell_x, double>(e, 0);
-        fill_march<gen::advec_cell_x, double, 0, 128, 1, 3>(e, 0);
+        fill_march<gen::advec_cell_x, double, 0, 128, 1, 128, 1, 3>(e, 0);
+        fill_march<gen::advec_cell_x, double, 0, 128, 1, 64, 1, 3>(e, 0);
+        fill_march<gen::advec_cell_x, double, 0, 64, 1, 64, 1, 4>(e, 0);
         register_entry(&e);
     }
 }

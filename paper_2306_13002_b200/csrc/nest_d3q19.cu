@@ -12,7 +12,10 @@ void register_d3q19() {
         e.function = "stream_collide";
         describe<gen::stream_collide>(e, "d3q19.c", 0);
         fill_naive<gen::stream_collide, double>(e, 0);
-        fill_march<gen::stream_collide, double, 1, 64, 4, 1>(e, 0);
+        fill_march<gen::stream_collide, double, 1, 64, 4, 64, 4, 1>(e, 0);
+        fill_march<gen::stream_collide, double, 1, 64, 2, 64, 2, 3>(e, 0);
+        fill_march<gen::stream_collide, double, 1, 32, 4, 32, 4, 3>(e, 0);
+        fill_march<gen::stream_collide, double, 1, 128, 2, 128, 2, 1>(e, 0);
         e.soa_last_dim = true;
         register_entry(&e);
     }

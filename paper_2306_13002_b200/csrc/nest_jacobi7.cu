@@ -12,7 +12,10 @@ void register_jacobi7() {
         e.function = "jacobi7";
         describe<gen::jacobi7>(e, "jacobi7.c", 0);
         fill_naive<gen::jacobi7, double>(e, 0);
-        fill_march<gen::jacobi7, double, 0, 64, 4, 3>(e, 0);
+        fill_march<gen::jacobi7, double, 0, 64, 4, 64, 4, 3>(e, 0);
+        fill_march<gen::jacobi7, double, 0, 64, 8, 64, 2, 3>(e, 0);
+        fill_march<gen::jacobi7, double, 0, 32, 16, 32, 4, 3>(e, 0);
+        fill_march<gen::jacobi7, double, 0, 128, 4, 128, 2, 2>(e, 0);
         register_entry(&e);
     }
 }

@@ -12,7 +12,9 @@ void register_swim() {
         e.function = "calc1";
         describe<gen::calc1>(e, "swim.c", 0);
         fill_naive<gen::calc1, double>(e, 0);
-        fill_march<gen::calc1, double, 0, 128, 1, 3>(e, 0);
+        fill_march<gen::calc1, double, 0, 128, 1, 128, 1, 3>(e, 0);
+        fill_march<gen::calc1, double, 0, 128, 1, 64, 1, 3>(e, 0);
+        fill_march<gen::calc1, double, 0, 64, 1, 64, 1, 4>(e, 0);
         register_entry(&e);
     }
     {
@@ -21,7 +23,9 @@ void register_swim() {
         e.function = "calc2";
         describe<gen::calc2>(e, "swim.c", 1);
         fill_naive<gen::calc2, double>(e, 0);
-        fill_march<gen::calc2, double, 0, 128, 1, 3>(e, 0);
+        fill_march<gen::calc2, double, 0, 128, 1, 128, 1, 3>(e, 0);
+        fill_march<gen::calc2, double, 0, 128, 1, 64, 1, 3>(e, 0);
+        fill_march<gen::calc2, double, 0, 64, 1, 64, 1, 4>(e, 0);
         register_entry(&e);
     }
     {
@@ -30,7 +34,9 @@ void register_swim() {
         e.function = "calc3";
         describe<gen::calc3>(e, "swim.c", 2);
         fill_naive<gen::calc3, double>(e, 0);
-        fill_march<gen::calc3, double, 0, 128, 1, 3>(e, 0);
+        fill_march<gen::calc3, double, 0, 128, 1, 128, 1, 3>(e, 0);
+        fill_march<gen::calc3, double, 0, 128, 1, 64, 1, 3>(e, 0);
+        fill_march<gen::calc3, double, 0, 64, 1, 64, 1, 4>(e, 0);
         register_entry(&e);
     }
 }

@@ -12,9 +12,12 @@ void register_wave4() {
         e.function = "wave4";
         describe<gen::wave4>(e, "wave4.c", 0);
         fill_naive<gen::wave4, double>(e, 0);
-        fill_march<gen::wave4, double, 0, 32, 8, 3>(e, 0);
+        fill_march<gen::wave4, double, 0, 32, 8, 32, 8, 3>(e, 0);
+        fill_march<gen::wave4, double, 0, 32, 16, 32, 4, 3>(e, 0);
         fill_naive<gen::wave4_f32, float>(e, 1);
-        fill_march<gen::wave4_f32, float, 0, 64, 8, 3>(e, 1);
+        fill_march<gen::wave4_f32, float, 0, 64, 8, 64, 8, 3>(e, 1);
+        fill_march<gen::wave4_f32, float, 0, 64, 8, 64, 2, 3>(e, 1);
+        fill_march<gen::wave4_f32, float, 0, 64, 16, 64, 4, 2>(e, 1);
         register_entry(&e);
     }
 }

@@ -27,8 +27,10 @@ struct LaunchReq {
 
 using LaunchFn = acs_status (*)(const LaunchReq&);
 
-// One registered region.  launch[precision][variant][schedule-1]; precision 0 =
-// the nest's declared type (double), 1 = the fp32 instantiation (wave4).
+// One registered region.  launch[precision][variant][slot]; precision 0 = the
+// nest's declared type (double), 1 = the fp32 instantiation (wave4); slot 0 =
+// the naive skeleton, slots 1.. = tiled (march) configurations.
+constexpr int kMaxSched = 8;
 struct Entry {
     std::string kernel_id, function;
     int region = 0;
@@ -37,7 +39,10 @@ struct Entry {
     std::vector<int> scalar_is_int;
     int static_loads[5] = {0, 0, 0, 0, 0};
     int fma_count[5] = {0, 0, 0, 0, 0};
-    LaunchFn launch[2][5][2] = {};
+    LaunchFn launch[2][5][kMaxSched] = {};
+    std::string sched_name[2][kMaxSched];
+    int n_sched[2] = {1, 1};     // slot 0 (naive) always present once registered
+    int best[2][5] = {};         // preferred slot per (precision, variant); acs_tune updates it
     bool soa_last_dim = false;   // backend layout: trailing component subscript made slowest (D3Q19 q)
     std::vector<int> component_last;  // per array: trailing subscript is an absolute component index
 };
@@ -171,6 +176,7 @@ void fill_naive(Entry& e, int prec) {
     e.launch[prec][2][0] = &launch_naive<NS, T, 2>;
     e.launch[prec][3][0] = &launch_naive<NS, T, 3>;
     e.launch[prec][4][0] = &launch_naive<NS, T, 4>;
+    e.sched_name[prec][0] = "naive (one thread per point, as-written loads for ORIGINAL)";
 }
 
 template <class NS>

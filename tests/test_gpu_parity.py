@@ -89,9 +89,10 @@ def cases():
     return out
 
 
-def schedules(kid):
+def schedules(kid, prec=0):
+    """Every registered schedule slot (0 = naive, 1.. = tiled configurations)."""
     k = backend.Kernel.lookup(kid)
-    return ["naive", "tiled"] if k.info["has_tiled"] else ["naive"]
+    return [i for i, name in enumerate(k.info["schedules"][prec]) if name]
 
 
 @pytest.mark.parametrize("kid,size", cases(), ids=[f"{k.split(':')[1]}-{s}" for k, s in cases()])
@@ -122,7 +123,7 @@ def test_wave4_fp32_parity(size, variant):
     ins = nests.make_inputs(w)
     want = {n: a.copy() for n, a in ins.items()}
     oracle_cpu.run(spec, want, w.scalars, variant, fma=variant in SAT, f32=True)
-    for sched in schedules(kid):
+    for sched in schedules(kid, prec=1):
         got = run_gpu(kid, ins, w.scalars, variant, sched)
         assert bitwise_equal(got["un"], want["un"]), f"wave4 fp32 {variant}/{sched} differs"
     # against the fp64 text: rel 1e-5 with a norm-wise floor
@@ -186,6 +187,20 @@ def test_device_fill_matches_host_inputs():
                 lo = fl.value if fl.kind == "const" else fl.lo
                 backend.fill(t, fl.kind, nests.SEED_BASE + p.position, lo, fl.hi, fl.p)
                 assert bitwise_equal(to_host(t), ins[p.name]), f"{kid}:{p.name}"
+
+
+def test_tune_picks_a_registered_slot_and_keeps_parity():
+    kid = "jacobi7.c:jacobi7:0"
+    w = nests.workload(kid, (20, 33, 70))
+    ins = nests.make_inputs(w)
+    k = backend.Kernel.lookup(kid)
+    dev = {n: to_device(k, n, a) for n, a in ins.items()}
+    best, ms = k.tune(dev, dict(w.scalars), "accsat", reps=2)
+    assert best in ms and len(ms) == len(schedules(kid))
+    want = {n: a.copy() for n, a in ins.items()}
+    oracle_cpu.run(w.spec, want, w.scalars, "accsat", fma=True)
+    got = run_gpu(kid, ins, w.scalars, "accsat", "default")
+    assert bitwise_equal(got["Anext"], want["Anext"])
 
 
 def test_errors_are_loud():
