@@ -124,6 +124,11 @@ def dist_setup(args):
         import torch.distributed as dist
         if args.impl == "reference":
             return rank, ws, local, None
+        if os.environ.get("ACS_BENCH_SAME_DEVICE"):
+            # functional check of the N-rank path on a one-GPU box (numbers meaningless)
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+            return rank, ws, 0, dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         return rank, ws, local, dist
@@ -226,6 +231,8 @@ def main():
     from paper_2306_13002_b200 import backend, nests
     rank, ws, local, dist = dist_setup(args)
     peak, peak_kind = load_peaks()
+    if ws > 1:
+        return main_sharded(args, rank, ws, local, dist, peak, peak_kind)
     kid = WORKLOAD_KID
     w = nests.workload(kid, args.size)
     k = backend.Kernel.lookup(kid)
@@ -288,6 +295,100 @@ def main():
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out))
+
+
+def main_sharded(args, rank, ws, local, dist, peak, peak_kind):
+    """N GPUs: the D3Q19 domain is slab-sharded along z, 256 planes per rank
+    (weak scaling: global grid 256 x 256 x 256N).  Each step every rank
+    computes its slab with the pushes that cross a slab face written straight
+    into the neighbour's distribution array over NVLink (CUDA IPC peer
+    memory, from inside the kernel), ordered by device-side flags."""
+    import torch
+    from paper_2306_13002_b200 import backend, nests, shard
+    kid = WORKLOAD_KID
+    size = (args.size * ws, args.size, args.size)
+    sr = shard.SlabRank(kid, size, ws, rank, variant=args.variant, schedule=args.schedule)
+    stream = torch.cuda.current_stream()
+    tuned = None
+    if args.schedule == "default" and args.variant != "original":
+        tuned, _ = sr.k.tune(sr.buf, dict(sr.w.scalars), args.variant, reps=3)   # untimed
+        sr.schedule = tuned
+        sr.refill()
+    torch.cuda.synchronize()
+    exp = [None] * ws
+    dist.all_gather_object(exp, sr.export())
+    sr.connect_ipc(exp[rank - 1] if rank > 0 else None, exp[rank + 1] if rank < ws - 1 else None)
+    dist.barrier()
+    launches = {"n": 0}
+
+    def step():
+        sr.step(stream=stream)
+        launches["n"] += 1 + (1 if sr.step_no > 1 and (sr.lo_ptr or sr.hi_ptr) else 0) + (1 if sr.lo_flag or sr.hi_flag else 0)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches["n"] = 0
+    with ClockSampler(local) as clk:
+        ms = time_steps(step, args.steps, 0, stream, dist)
+    local_bytes = sr.w.algorithmic_bytes
+    value = ws * local_bytes / (ms * 1e-3) / 1e9
+    out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded SplitMix64, SURVEY.md §8d distributions; generated in HBM)",
+           "config": {"workload": "D3Q19 lattice-Boltzmann collide+stream (olbm-like) fp64, one sweep per step",
+                      "grid": [args.size, args.size, args.size * ws], "per_rank_grid": [args.size] * 3,
+                      "form": args.variant, "schedule": args.schedule, "tuned_slot": tuned,
+                      "parallelism": f"z-slab sharding x{ws}, fused peer-memory push exchange + device flags",
+                      "layout": "q-major SoA in HBM", "l2": "inputs >> L2 (no flush needed)",
+                      "bytes_per_point": sr.w.bytes_per_point},
+           "gpu_launches": launches["n"]}
+    achieved = local_bytes / (ms * 1e-3) / 1e9
+    out["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                       "frac": round(achieved / peak, 4), "peak_kind": peak_kind, "traffic": load_traffic("stream_collide"),
+                       "kernel": "stream_collide " + args.variant + " (sharded, per rank)"}
+    out["clocks"] = clk.summary()
+    if not args.no_e2e:
+        out["e2e"] = e2e_sharded(args, sr, dist, ws)
+    sr.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out))
+    return 0
+
+
+def e2e_sharded(args, sr, dist, ws):
+    """Per rank per step: its slab's reference-layout host buffers -> device ->
+    remap -> sharded step (with the peer exchange) -> remap -> host."""
+    import torch
+    from paper_2306_13002_b200 import backend, shard
+    stream = torch.cuda.current_stream()
+    names = [a.name for a in sr.w.spec.arrays]
+    host = {n: torch.empty(tuple(sr.buf[n].shape), dtype=sr.buf[n].dtype, pin_memory=True) for n in names}
+    rm = {n: torch.empty(tuple(sr.buf[n].shape), dtype=sr.buf[n].dtype, device="cuda") for n in names}
+    for n in names:
+        backend.copy(rm[n], sr.buf[n])
+        host[n].copy_(rm[n])
+    torch.cuda.synchronize()
+
+    def step():
+        roles = shard.role_buffers(sr.nest, names, sr.step_no)
+        for p in names:
+            rm[p].copy_(host[p], non_blocking=True)
+            backend.copy(sr.buf[roles[p]], rm[p], stream)
+        sr.step(stream=stream)
+        backend.copy(rm["dst"], sr.buf[roles["dst"]], stream)
+        host["dst"].copy_(rm["dst"], non_blocking=True)
+
+    steps = max(3, min(args.steps, 10))
+    ms = time_steps(step, steps, 2, stream, dist)
+    h2d = sum(host[n].numel() * host[n].element_size() for n in names)
+    d2h = host["dst"].numel() * host["dst"].element_size()
+    return {"value": round(ws * sr.w.algorithmic_bytes / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3), "steps": steps,
+            "path": "per rank: pinned host slab (reference AoS) -> H2D -> remap -> sharded acs_launch -> remap -> D2H"}
 
 
 def load_traffic(kernel_name):

@@ -135,13 +135,55 @@ acs_status acs_tune(const acs_kernel* k, acs_variant variant, const acs_array* a
                     const acs_scalar* scalars, int n_scalars, void* cuda_stream, int reps, int* best_slot,
                     float* ms_per_launch);
 
+/* ---- slab sharding across GPUs -------------------------
+ * Each rank owns planes [own_lo, own_hi) (global coordinates) of the outermost
+ * loop; its buffers hold those planes plus halos, local index 0 = global
+ * `origin`.  Owner computes; every store of a listed array to global plane g
+ * is ALSO written, from inside the same kernel, into the lower neighbour's
+ * buffer when g < own_lo + halo and into the upper neighbour's when
+ * g >= own_hi - halo (peer device memory: NVLink P2P, or the same device).
+ * `halo` is how far beyond its owned range the NEXT step reads the produced
+ * data (wave4: 2, jacobi7: 1, D3Q19 push-stream: 0 — only pushes into the
+ * neighbour's planes travel).  Order steps across ranks with acs_signal /
+ * acs_wait (device-side release/acquire flags, no host round trip).
+ * Neighbours' buffers must have the same element strides as this rank's
+ * (allocate every slab with the same plane count; use views for the rest). */
+#define ACS_MAX_SHARDED 16
+typedef struct {
+    int64_t own_lo, own_hi;
+    int64_t origin;
+    int32_t halo;
+    int32_t n_sharded;
+    const char* names[ACS_MAX_SHARDED];   /* arrays whose stores are written through */
+    void* lo_data[ACS_MAX_SHARDED];       /* lower neighbour's buffer of names[i] (NULL: none) */
+    void* hi_data[ACS_MAX_SHARDED];       /* upper neighbour's buffer (NULL: none) */
+    int64_t lo_origin, hi_origin;         /* neighbours' `origin` */
+} acs_shard;
+
+acs_status acs_launch_sharded(const acs_kernel* k, acs_variant variant, acs_schedule schedule,
+                              const acs_array* arrays, int n_arrays, const acs_scalar* scalars, int n_scalars,
+                              const acs_shard* shard, void* cuda_stream);
+/* stream-ordered: after all prior work on the stream, system-scope release
+ * store of `value` into each non-NULL flag (peer or local device memory) */
+acs_status acs_signal(uint64_t* flag_a, uint64_t* flag_b, uint64_t value, void* cuda_stream);
+/* stream-ordered: block the stream until each non-NULL local flag >= value
+ * (acquire); traps after `timeout_ms` so a lost peer is a loud error, not a hang */
+acs_status acs_wait(const uint64_t* flag_a, const uint64_t* flag_b, uint64_t value, int timeout_ms,
+                    void* cuda_stream);
+/* CUDA IPC of a device pointer inside any allocation (base handle + offset) */
+acs_status acs_ipc_export(const void* dptr, void* handle_out /* 64 bytes */, int64_t* offset_out);
+acs_status acs_ipc_import(const void* handle /* 64 bytes */, int64_t offset, void** dptr_out);
+acs_status acs_ipc_close(void* dptr, int64_t offset);
+
 /* Device data utilities (synthetic inputs, layout remaps). */
 typedef enum { ACS_FILL_UNIFORM = 0, ACS_FILL_CONST = 1, ACS_FILL_MASK = 2, ACS_FILL_D3Q19 = 3 } acs_fill_kind;
 /* Fills a (possibly strided) array.  Element at reference flat index f gets
- * SplitMix64(seed, f): UNIFORM lo+(hi-lo)*u, CONST lo, MASK (u < p), D3Q19
- * w[f % 19] * (1 + (lo+(hi-lo)*u)).  Bit-identical to nests.make_inputs. */
+ * SplitMix64(seed, f + flat_offset): UNIFORM lo+(hi-lo)*u, CONST lo, MASK
+ * (u < p), D3Q19 w[f % 19] * (1 + (lo+(hi-lo)*u)).  Bit-identical to
+ * nests.make_inputs; flat_offset lets a slab reproduce its part of a global
+ * array. */
 acs_status acs_fill(const acs_array* a, acs_fill_kind kind, uint64_t seed, double lo, double hi,
-                    double p, void* cuda_stream);
+                    double p, int64_t flat_offset, void* cuda_stream);
 /* Strided element copy between two arrays of the same dims (any strides,
  * dtype conversion between integer types or between real types). */
 acs_status acs_copy(const acs_array* dst, const acs_array* src, void* cuda_stream);

@@ -79,7 +79,7 @@ EXPORTS = {
                                 ctypes.POINTER(AcsScalar), ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
                                 ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_float)]),
     "acs_fill": (ctypes.c_int, [ctypes.POINTER(AcsArray), ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
-                                ctypes.c_double, ctypes.c_double, ctypes.c_void_p]),
+                                ctypes.c_double, ctypes.c_double, ctypes.c_int64, ctypes.c_void_p]),
     "acs_copy": (ctypes.c_int, [ctypes.POINTER(AcsArray), ctypes.POINTER(AcsArray), ctypes.c_void_p]),
     "acs_native_strides": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int,
                                           ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
@@ -214,9 +214,13 @@ class Kernel:
         return tuple(s)
 
 
-def fill(t, kind: str, seed: int, lo: float = 0.0, hi: float = 1.0, p: float = 0.0, stream=None) -> None:
+def fill(t, kind: str, seed: int, lo: float = 0.0, hi: float = 1.0, p: float = 0.0, stream=None,
+         flat_offset: int = 0) -> None:
+    """acs_fill; `flat_offset` = reference flat index of t's first element
+    within a larger (global) array, so a slab reproduces its share."""
     a = describe("fill", t)
-    _check(lib().acs_fill(ctypes.byref(a), FILL[kind], seed, lo, hi, p, _stream_handle(stream)), "acs_fill")
+    _check(lib().acs_fill(ctypes.byref(a), FILL[kind], seed, lo, hi, p, flat_offset, _stream_handle(stream)),
+           "acs_fill")
 
 
 def copy(dst, src, stream=None) -> None:

@@ -10,6 +10,8 @@
 #include "registry.hpp"
 #include "tma.cuh"
 
+#include <cstring>
+
 namespace acs {
 
 void register_jacobi7();
@@ -83,7 +85,7 @@ __device__ __forceinline__ long long strided_offset(const StridedDesc& d, long l
 
 template <class T>
 __global__ void fill_kernel(T* base, StridedDesc d, long long n, int kind, uint64_t seed, double lo, double hi,
-                            double p) {
+                            double p, long long off) {
     const double span = __dsub_rn(hi, lo);
     const double w[3] = {1.0 / 3.0, 1.0 / 18.0, 1.0 / 36.0};
     for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < n; f += (long long)gridDim.x * blockDim.x) {
@@ -91,13 +93,13 @@ __global__ void fill_kernel(T* base, StridedDesc d, long long n, int kind, uint6
         if (kind == ACS_FILL_CONST) {
             v = lo;
         } else {
-            const double u = (double)(splitmix64(seed, (uint64_t)f) >> 11) * 0x1.0p-53;
+            const double u = (double)(splitmix64(seed, (uint64_t)(f + off)) >> 11) * 0x1.0p-53;
             if (kind == ACS_FILL_MASK) {
                 v = u < p ? 1.0 : 0.0;
             } else {
                 const double x = __dadd_rn(lo, __dmul_rn(span, u));
                 if (kind == ACS_FILL_D3Q19) {
-                    const int q = (int)(f % 19);
+                    const int q = (int)((f + off) % 19);
                     v = __dmul_rn(w[q == 0 ? 0 : (q <= 6 ? 1 : 2)], __dadd_rn(1.0, x));
                 } else {
                     v = x;
@@ -110,7 +112,7 @@ __global__ void fill_kernel(T* base, StridedDesc d, long long n, int kind, uint6
 
 template <>
 __global__ void fill_kernel<float>(float* base, StridedDesc d, long long n, int kind, uint64_t seed, double lo,
-                                   double hi, double p) {
+                                   double hi, double p, long long off) {
     const double span = __dsub_rn(hi, lo);
     const double w[3] = {1.0 / 3.0, 1.0 / 18.0, 1.0 / 36.0};
     for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < n; f += (long long)gridDim.x * blockDim.x) {
@@ -118,10 +120,11 @@ __global__ void fill_kernel<float>(float* base, StridedDesc d, long long n, int 
         if (kind == ACS_FILL_CONST) {
             v = lo;
         } else {
-            const double u = (double)(splitmix64(seed, (uint64_t)f) >> 11) * 0x1.0p-53;
+            const double u = (double)(splitmix64(seed, (uint64_t)(f + off)) >> 11) * 0x1.0p-53;
             const double x = __dadd_rn(lo, __dmul_rn(span, u));
+            const int q = (int)((f + off) % 19);
             v = kind == ACS_FILL_MASK ? (u < p ? 1.0 : 0.0)
-                : kind == ACS_FILL_D3Q19 ? __dmul_rn(w[(f % 19) == 0 ? 0 : ((f % 19) <= 6 ? 1 : 2)], __dadd_rn(1.0, x))
+                : kind == ACS_FILL_D3Q19 ? __dmul_rn(w[q == 0 ? 0 : (q <= 6 ? 1 : 2)], __dadd_rn(1.0, x))
                 : x;
         }
         base[strided_offset(d, f)] = __double2float_rn(v);
@@ -170,6 +173,37 @@ int grid_for(long long n) {
 }  // namespace acs
 
 using namespace acs;
+
+typedef CUresult (*GetAddressRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+static acs_status launch_impl(const acs_kernel* k, acs_variant variant, acs_schedule schedule, const acs_array* arrays,
+                              int n_arrays, const acs_scalar* scalars, int n_scalars, const acs_shard* shard,
+                              void* cuda_stream);
+
+// stream-ordered cross-rank step flags (release / acquire at system scope)
+__global__ void signal_kernel(unsigned long long* a, unsigned long long* b, unsigned long long v) {
+    __threadfence_system();   // this stream's earlier kernels' stores (incl. peer stores) before the flag
+    if (a) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+    if (b) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(b), "l"(v) : "memory");
+}
+
+__global__ void wait_kernel(const unsigned long long* a, const unsigned long long* b, unsigned long long v,
+                            unsigned long long timeout_ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (const unsigned long long* f : {a, b}) {
+        if (!f) continue;
+        for (;;) {
+            unsigned long long x;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(f) : "memory");
+            if (x >= v) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > timeout_ns) __trap();   // a peer never arrived: fail loudly
+            __nanosleep(200);
+        }
+    }
+    __threadfence_system();
+}
 
 extern "C" {
 
@@ -242,6 +276,14 @@ int acs_kernel_scalar_is_int(const acs_kernel* k, int index) {
 
 acs_status acs_launch(const acs_kernel* k, acs_variant variant, acs_schedule schedule, const acs_array* arrays,
                       int n_arrays, const acs_scalar* scalars, int n_scalars, void* cuda_stream) {
+    return launch_impl(k, variant, schedule, arrays, n_arrays, scalars, n_scalars, nullptr, cuda_stream);
+}
+
+}  // extern "C"
+
+static acs_status launch_impl(const acs_kernel* k, acs_variant variant, acs_schedule schedule, const acs_array* arrays,
+                              int n_arrays, const acs_scalar* scalars, int n_scalars, const acs_shard* shard,
+                              void* cuda_stream) {
     if (!k || (n_arrays > 0 && !arrays) || (n_scalars > 0 && !scalars)) {
         set_error("acs_launch: null argument");
         return ACS_E_ARG;
@@ -267,8 +309,94 @@ acs_status acs_launch(const acs_kernel* k, acs_variant variant, acs_schedule sch
                   std::to_string(variant) + (prec ? " (fp32)" : ""));
         return ACS_E_NO_KERNEL;
     }
-    LaunchReq r{arrays, n_arrays, scalars, n_scalars, static_cast<cudaStream_t>(cuda_stream)};
+    LaunchReq r{arrays, n_arrays, scalars, n_scalars, static_cast<cudaStream_t>(cuda_stream), shard};
     return fn(r);
+}
+
+extern "C" {
+
+acs_status acs_launch_sharded(const acs_kernel* k, acs_variant variant, acs_schedule schedule, const acs_array* arrays,
+                              int n_arrays, const acs_scalar* scalars, int n_scalars, const acs_shard* shard,
+                              void* cuda_stream) {
+    if (!shard || shard->n_sharded < 0 || shard->n_sharded > ACS_MAX_SHARDED || shard->own_hi < shard->own_lo ||
+        shard->halo < 0) {
+        set_error("acs_launch_sharded: bad shard descriptor");
+        return ACS_E_ARG;
+    }
+    return launch_impl(k, variant, schedule, arrays, n_arrays, scalars, n_scalars, shard, cuda_stream);
+}
+
+acs_status acs_signal(uint64_t* flag_a, uint64_t* flag_b, uint64_t value, void* cuda_stream) {
+    signal_kernel<<<1, 1, 0, static_cast<cudaStream_t>(cuda_stream)>>>((unsigned long long*)flag_a,
+                                                                      (unsigned long long*)flag_b, value);
+    return check_launch("acs_signal");
+}
+
+acs_status acs_wait(const uint64_t* flag_a, const uint64_t* flag_b, uint64_t value, int timeout_ms, void* cuda_stream) {
+    wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(cuda_stream)>>>((const unsigned long long*)flag_a,
+                                                                    (const unsigned long long*)flag_b, value,
+                                                                    (unsigned long long)timeout_ms * 1000000ULL);
+    return check_launch("acs_wait");
+}
+
+acs_status acs_ipc_export(const void* dptr, void* handle_out, int64_t* offset_out) {
+    if (!dptr || !handle_out || !offset_out) {
+        set_error("acs_ipc_export: null argument");
+        return ACS_E_ARG;
+    }
+    static GetAddressRangeFn range = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (GetAddressRangeFn) nullptr;
+        return reinterpret_cast<GetAddressRangeFn>(p);
+    }();
+    if (!range) {
+        set_error("acs_ipc_export: cuMemGetAddressRange unavailable");
+        return ACS_E_NCCL;
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dptr)) != CUDA_SUCCESS) {
+        set_error("acs_ipc_export: not a device allocation");
+        return ACS_E_ARG;
+    }
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+        return ACS_E_CUDA;
+    }
+    std::memcpy(handle_out, &h, sizeof h);
+    *offset_out = (int64_t)(reinterpret_cast<CUdeviceptr>(dptr) - base);
+    return ACS_OK;
+}
+
+acs_status acs_ipc_import(const void* handle, int64_t offset, void** dptr_out) {
+    if (!handle || !dptr_out) {
+        set_error("acs_ipc_import: null argument");
+        return ACS_E_ARG;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+        return ACS_E_CUDA;
+    }
+    *dptr_out = static_cast<char*>(base) + offset;
+    return ACS_OK;
+}
+
+acs_status acs_ipc_close(void* dptr, int64_t offset) {
+    cudaError_t e = cudaIpcCloseMemHandle(static_cast<char*>(dptr) - offset);
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaIpcCloseMemHandle: ") + cudaGetErrorString(e));
+        return ACS_E_CUDA;
+    }
+    return ACS_OK;
 }
 
 const char* acs_kernel_schedule_name(const acs_kernel* k, int precision, int slot) {
@@ -333,7 +461,7 @@ acs_status acs_tune(const acs_kernel* k, acs_variant variant, const acs_array* a
 }
 
 acs_status acs_fill(const acs_array* a, acs_fill_kind kind, uint64_t seed, double lo, double hi, double p,
-                    void* cuda_stream) {
+                    int64_t flat_offset, void* cuda_stream) {
     StridedDesc d;
     long long n;
     if (!make_desc(a, d, n)) {
@@ -343,10 +471,10 @@ acs_status acs_fill(const acs_array* a, acs_fill_kind kind, uint64_t seed, doubl
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     const int g = grid_for(n);
     switch (a->dtype) {
-        case ACS_F64: fill_kernel<double><<<g, 256, 0, s>>>((double*)a->data, d, n, kind, seed, lo, hi, p); break;
-        case ACS_F32: fill_kernel<float><<<g, 256, 0, s>>>((float*)a->data, d, n, kind, seed, lo, hi, p); break;
-        case ACS_I32: fill_kernel<int><<<g, 256, 0, s>>>((int*)a->data, d, n, kind, seed, lo, hi, p); break;
-        case ACS_U8: fill_kernel<uint8_t><<<g, 256, 0, s>>>((uint8_t*)a->data, d, n, kind, seed, lo, hi, p); break;
+        case ACS_F64: fill_kernel<double><<<g, 256, 0, s>>>((double*)a->data, d, n, kind, seed, lo, hi, p, (long long)flat_offset); break;
+        case ACS_F32: fill_kernel<float><<<g, 256, 0, s>>>((float*)a->data, d, n, kind, seed, lo, hi, p, (long long)flat_offset); break;
+        case ACS_I32: fill_kernel<int><<<g, 256, 0, s>>>((int*)a->data, d, n, kind, seed, lo, hi, p, (long long)flat_offset); break;
+        case ACS_U8: fill_kernel<uint8_t><<<g, 256, 0, s>>>((uint8_t*)a->data, d, n, kind, seed, lo, hi, p, (long long)flat_offset); break;
         default: set_error("acs_fill: unsupported dtype"); return ACS_E_ARG;
     }
     return check_launch("acs_fill");

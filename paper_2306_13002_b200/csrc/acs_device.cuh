@@ -24,12 +24,28 @@ struct ArrayView {
     long long stride[8];   // element strides per subscript position
 };
 
+// Slab sharding (owner computes, write-through to every holder): a store to
+// global plane g of a sharded array is also written straight into the lower
+// neighbour's buffer when g < lo_thr and into the upper neighbour's when
+// g >= hi_thr (peer memory over NVLink, or the same device).  dlo/dhi are the
+// element offsets from this rank's buffer index to the neighbour's.
+template <int NARR>
+struct ShardArgs {
+    int enabled;
+    long long origin;    // global coordinate of local index 0 along subscript 0
+    long long lo_thr, hi_thr;
+    char* peer_lo[NARR];
+    char* peer_hi[NARR];
+    long long dlo[NARR], dhi[NARR];
+};
+
 template <class NS>
 struct KernelArgs {
     ArrayView arr[NS::NARR];
     typename NS::Scalars s;
     int lo[NS::NLOOP];
     int hi[NS::NLOOP];
+    ShardArgs<NS::NARR> sh;
 };
 
 // ---- raw access primitives ------------------------------------------------
@@ -121,8 +137,27 @@ struct NaiveMem {
     __device__ __forceinline__ elem_t<ARR> ld() const { return load_at<ARR>(static_index<ARR, O...>()); }
     template <int ARR, class... I>
     __device__ __forceinline__ elem_t<ARR> ldx(I... idx) const { return load_at<ARR>(dyn_index<ARR>(idx...)); }
+    // write-through of a store to the neighbours that hold plane l0 (sharded launches)
+    template <int ARR>
+    __device__ __forceinline__ void forward(long long idx, long long l0, elem_t<ARR> v) const {
+        const long long g = l0 + a.sh.origin;
+        if (g < a.sh.lo_thr && a.sh.peer_lo[ARR])
+            *(reinterpret_cast<elem_t<ARR>*>(a.sh.peer_lo[ARR]) + idx + a.sh.dlo[ARR]) = v;
+        if (g >= a.sh.hi_thr && a.sh.peer_hi[ARR])
+            *(reinterpret_cast<elem_t<ARR>*>(a.sh.peer_hi[ARR]) + idx + a.sh.dhi[ARR]) = v;
+    }
+
     template <int ARR, int... O>
-    __device__ __forceinline__ void st(elem_t<ARR> v) const { store_at<ARR>(static_index<ARR, O...>(), v); }
+    __device__ __forceinline__ void st(elem_t<ARR> v) const {
+        const long long idx = static_index<ARR, O...>();
+        store_at<ARR>(idx, v);
+        if constexpr (NS::sig(ARR, 0) == 0) {
+            if (a.sh.enabled) {
+                constexpr int off[sizeof...(O)] = {O...};
+                forward<ARR>(idx, (long long)pt[0] + off[0], v);
+            }
+        }
+    }
     template <int ARR, class... A>
     __device__ __forceinline__ void stx(A... args) const {
         // last argument is the value; the rest are subscripts
@@ -131,24 +166,29 @@ struct NaiveMem {
 
   private:
     template <int ARR, class I0, class V>
-    __device__ __forceinline__ void stx_impl(I0 i0, V v) const { store_at<ARR>(dyn_index<ARR>(i0), v); }
+    __device__ __forceinline__ void stx_at(long long idx, I0 i0, V v) const {
+        store_at<ARR>(idx, v);
+        if (a.sh.enabled) forward<ARR>(idx, (long long)i0, v);
+    }
+    template <int ARR, class I0, class V>
+    __device__ __forceinline__ void stx_impl(I0 i0, V v) const { stx_at<ARR>(dyn_index<ARR>(i0), i0, v); }
     template <int ARR, class I0, class I1, class V>
-    __device__ __forceinline__ void stx_impl(I0 i0, I1 i1, V v) const { store_at<ARR>(dyn_index<ARR>(i0, i1), v); }
+    __device__ __forceinline__ void stx_impl(I0 i0, I1 i1, V v) const { stx_at<ARR>(dyn_index<ARR>(i0, i1), i0, v); }
     template <int ARR, class I0, class I1, class I2, class V>
     __device__ __forceinline__ void stx_impl(I0 i0, I1 i1, I2 i2, V v) const {
-        store_at<ARR>(dyn_index<ARR>(i0, i1, i2), v);
+        stx_at<ARR>(dyn_index<ARR>(i0, i1, i2), i0, v);
     }
     template <int ARR, class I0, class I1, class I2, class I3, class V>
     __device__ __forceinline__ void stx_impl(I0 i0, I1 i1, I2 i2, I3 i3, V v) const {
-        store_at<ARR>(dyn_index<ARR>(i0, i1, i2, i3), v);
+        stx_at<ARR>(dyn_index<ARR>(i0, i1, i2, i3), i0, v);
     }
 };
 
 // One thread per point of the marked loop nest: innermost loop on x, the next
 // on y, the outermost (3-D nests) on z — the gang/worker/vector mapping of the
 // nest's own directives.
-template <class NS, class T, int FORM, bool ASIS>
-__global__ void __launch_bounds__(256) naive_kernel(const __grid_constant__ KernelArgs<NS> args) {
+template <class NS, class T, int FORM, bool ASIS, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) naive_kernel(const __grid_constant__ KernelArgs<NS> args) {
     constexpr int NL = NS::NLOOP;
     int pt[NL];
     const int x = args.lo[NL - 1] + (int)(blockIdx.x * blockDim.x + threadIdx.x);

@@ -195,41 +195,39 @@ struct MarchMem {
         }
     }
 
+    // out-of-box dynamic index: rare (e.g. advec's clamp at the domain edge),
+    // kept out of line so the in-box path stays a few integer ops + one LDS
+    template <int ARR, class... I>
+    __device__ __noinline__ elem_t<ARR> ldx_global(I... ii) const { return g.template ldx<ARR>(ii...); }
+
     template <int ARR, class... I>
     __device__ __forceinline__ elem_t<ARR> ldx(I... ii) const {
         if constexpr (P::staged(ARR)) {
             const int v[sizeof...(I)] = {(int)ii...};
             int idx = 0, delta = 0;
-            bool in = true;
+            unsigned out = 0;
 #pragma unroll
             for (int p = 0; p < (int)sizeof...(I); ++p) {
                 const int s = NS::ld_sig(ARR, p);
                 const int lo = NS::ld_lo(ARR, p);
-                int l;
                 if (s == 0) {
                     const int d = v[p] - k;
-                    in = in && d >= lo && d <= NS::ld_hi(ARR, p);
+                    out |= (unsigned)(d - lo) > (unsigned)(NS::ld_hi(ARR, p) - lo);
                     delta = D + d - NS::ld_hi(ARR, p);
-                    continue;
-                } else if (s == P::X) {
-                    l = v[p] - orgx - lo;
-                    in = in && l >= 0 && l < P::raw_extent(ARR, p);
-                    idx += (l + sh[ARR]) * P::bstride(ARR, p);
-                    continue;
-                } else if (s == P::Y) {
-                    l = v[p] - orgy - lo;
                 } else {
-                    l = v[p] - lo;
+                    const int l = v[p] - lo - (s == P::X ? orgx : (s == P::Y ? orgy : 0));
+                    out |= (unsigned)l >= (unsigned)P::raw_extent(ARR, p);
+                    idx += (l + (s == P::X ? sh[ARR] : 0)) * P::bstride(ARR, p);
                 }
-                in = in && l >= 0 && l < P::raw_extent(ARR, p);
-                idx += l * P::bstride(ARR, p);
             }
-            if (in) {
+            if (__builtin_expect(out == 0, 1)) {
                 if (delta >= D) delta -= D;
                 return box_base<ARR>(delta)[idx];
             }
+            return ldx_global<ARR>(ii...);
+        } else {
+            return g.template ldx<ARR>(ii...);
         }
-        return g.template ldx<ARR>(ii...);
     }
     template <int ARR, int... O>
     __device__ __forceinline__ void st(elem_t<ARR> v) const { g.template st<ARR, O...>(v); }

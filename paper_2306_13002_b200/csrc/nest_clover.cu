@@ -1,6 +1,7 @@
 // Registration of the clover nest functions (generated bodies: gen/clover.cuh).
 #include "registry.hpp"
 #include "kernels/march.cuh"
+#include "kernels/stream.cuh"
 #include "gen/clover.cuh"
 
 namespace acs {
@@ -12,6 +13,8 @@ void register_clover() {
         e.function = "ideal_gas";
         describe<gen::ideal_gas>(e, "clover.c", 0);
         fill_naive<gen::ideal_gas, double>(e, 0);
+        fill_stream<gen::ideal_gas, double, 128, 3>(e, 0);
+        fill_stream<gen::ideal_gas, double, 256, 4>(e, 0);
         fill_march<gen::ideal_gas, double, 0, 128, 1, 128, 1, 3>(e, 0);
         fill_march<gen::ideal_gas, double, 0, 128, 1, 64, 1, 3>(e, 0);
         fill_march<gen::ideal_gas, double, 0, 64, 1, 64, 1, 4>(e, 0);

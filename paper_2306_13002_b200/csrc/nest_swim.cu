@@ -1,6 +1,7 @@
 // Registration of the swim nest functions (generated bodies: gen/swim.cuh).
 #include "registry.hpp"
 #include "kernels/march.cuh"
+#include "kernels/stream.cuh"
 #include "gen/swim.cuh"
 
 namespace acs {
@@ -34,6 +35,8 @@ void register_swim() {
         e.function = "calc3";
         describe<gen::calc3>(e, "swim.c", 2);
         fill_naive<gen::calc3, double>(e, 0);
+        fill_stream<gen::calc3, double, 128, 3>(e, 0);
+        fill_stream<gen::calc3, double, 256, 4>(e, 0);
         fill_march<gen::calc3, double, 0, 128, 1, 128, 1, 3>(e, 0);
         fill_march<gen::calc3, double, 0, 128, 1, 64, 1, 3>(e, 0);
         fill_march<gen::calc3, double, 0, 64, 1, 64, 1, 4>(e, 0);

@@ -23,6 +23,7 @@ struct LaunchReq {
     const acs_scalar* scalars;
     int n_scalars;
     cudaStream_t stream;
+    const acs_shard* shard = nullptr;   // slab-sharded launch (acs_launch_sharded)
 };
 
 using LaunchFn = acs_status (*)(const LaunchReq&);
@@ -110,6 +111,31 @@ acs_status bind(const LaunchReq& r, KernelArgs<NS>& ka, bool& empty) {
         const double dv = d->is_int ? (double)d->i : d->d;
         NS::set_scalar(ka.s, s, iv, dv);
     }
+    std::memset(&ka.sh, 0, sizeof ka.sh);
+    if (r.shard) {
+        const acs_shard& sd = *r.shard;
+        ka.sh.enabled = 1;
+        ka.sh.origin = sd.origin;
+        ka.sh.lo_thr = sd.own_lo + sd.halo;
+        ka.sh.hi_thr = sd.own_hi - sd.halo;
+        for (int i = 0; i < sd.n_sharded; ++i) {
+            int a = -1;
+            for (int b = 0; b < NS::NARR; ++b)
+                if (sd.names[i] && std::strcmp(sd.names[i], NS::array_names[b]) == 0) a = b;
+            if (a < 0) {
+                set_error(std::string("shard: unknown array '") + (sd.names[i] ? sd.names[i] : "") + "'");
+                return ACS_E_ARG;
+            }
+            if (NS::sig(a, 0) != 0 && NS::sig(a, 0) != -1) {
+                set_error(std::string("shard: array '") + NS::array_names[a] + "' is not sliced along the outer loop");
+                return ACS_E_ARG;
+            }
+            ka.sh.peer_lo[a] = static_cast<char*>(sd.lo_data[i]);
+            ka.sh.peer_hi[a] = static_cast<char*>(sd.hi_data[i]);
+            ka.sh.dlo[a] = (sd.origin - sd.lo_origin) * ka.arr[a].stride[0];
+            ka.sh.dhi[a] = (sd.origin - sd.hi_origin) * ka.arr[a].stride[0];
+        }
+    }
     long long lo[NS::NLOOP], hi[NS::NLOOP];
     NS::bounds(ka.s, lo, hi);
     empty = false;
@@ -143,7 +169,7 @@ inline acs_status check_launch(const char* what) {
     return ACS_OK;
 }
 
-template <class NS, class T, int FORM>
+template <class NS, class T, int FORM, int MINB = 1>
 acs_status launch_naive(const LaunchReq& r) {
     KernelArgs<NS> ka;
     bool empty = false;
@@ -165,7 +191,7 @@ acs_status launch_naive(const LaunchReq& r) {
     }
     // ORIGINAL keeps every as-written load and store (ld_asis); the emitted
     // forms use ordinary (read-only-path where legal) accesses.
-    naive_kernel<NS, T, FORM, FORM == ACS_ORIGINAL><<<grid, block, 0, r.stream>>>(ka);
+    naive_kernel<NS, T, FORM, FORM == ACS_ORIGINAL, MINB><<<grid, block, 0, r.stream>>>(ka);
     return check_launch(NS::array_names[0]);
 }
 
@@ -177,6 +203,20 @@ void fill_naive(Entry& e, int prec) {
     e.launch[prec][3][0] = &launch_naive<NS, T, 3>;
     e.launch[prec][4][0] = &launch_naive<NS, T, 4>;
     e.sched_name[prec][0] = "naive (one thread per point, as-written loads for ORIGINAL)";
+}
+
+// Extra naive slot with an occupancy floor: __launch_bounds__(256, MINB) caps
+// registers so MINB CTAs (8*MINB warps) fit per SM — more loads in flight
+// for register-heavy point-local nests (D3Q19).
+template <class NS, class T, int MINB>
+void fill_naive_occ(Entry& e, int prec) {
+    const int slot = e.n_sched[prec]++;
+    e.launch[prec][0][slot] = &launch_naive<NS, T, 0, MINB>;
+    e.launch[prec][1][slot] = &launch_naive<NS, T, 1, MINB>;
+    e.launch[prec][2][slot] = &launch_naive<NS, T, 2, MINB>;
+    e.launch[prec][3][slot] = &launch_naive<NS, T, 3, MINB>;
+    e.launch[prec][4][slot] = &launch_naive<NS, T, 4, MINB>;
+    e.sched_name[prec][slot] = "naive, >= " + std::to_string(MINB) + " CTAs/SM";
 }
 
 template <class NS>

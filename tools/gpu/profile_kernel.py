@@ -10,6 +10,7 @@ import torch  # noqa: E402
 from paper_2306_13002_b200 import backend, nests  # noqa: E402
 
 kid, variant, sched = sys.argv[1], sys.argv[2], sys.argv[3]
+sched = int(sched) - 16 if sched.isdigit() and int(sched) >= 16 else (int(sched) if sched.isdigit() else sched)
 dtype = "f32" if len(sys.argv) > 4 and sys.argv[4] == "f32" else "f64"
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 4
 w = nests.workload(kid, None, dtype=dtype)
