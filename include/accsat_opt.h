@@ -1,0 +1,50 @@
+/*
+ * accsat_opt.h — host stage (a): the compile-time optimizer that produces the
+ * saturated form the B200 kernels execute, re-implemented in C++ for the
+ * host.
+ *
+ * Replaces, with the same inputs, outputs and metrics:
+ *   optimize_source(source, name, VariantConfig, PipelineLimits)
+ *       (proj/include/satcc/pipeline.hpp:64-66, proj/src/pipeline.cpp:140-194)
+ * i.e. parse -> find_regions -> per region: value-numbered SSA with per-base
+ * load epochs and same-scope store->load forwarding (proj/src/ssa.cpp) ->
+ * e-graph (hash-consing = load CSE, proj/src/egraph.cpp) -> [saturation with
+ * the nine Table-I rules + constant folding, proj/src/rules.cpp:123-251] ->
+ * extraction under the same cost model (const 0 / leaf 1 / op 10 /
+ * load-div-mod-call 100, proj/src/cost.cpp:9-41) -> depth-one temps and
+ * [bulk load motion] -> re-emitted module text.  Fail-open per region.
+ *
+ * Differences by design: extraction is greedy tree-cost followed by an exact
+ * incremental DAG-cost local search (no 30 s branch-and-bound timeout), so a
+ * region optimizes in milliseconds; results are checked against the frozen
+ * reference outputs for objective, load count and semantics
+ * (tests/test_opt.py).
+ */
+#ifndef ACCSAT_OPT_H
+#define ACCSAT_OPT_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+    long max_nodes;        /* saturation node budget (reference default 10000) */
+    double max_time_s;     /* saturation wall-time budget (default 10) */
+    int max_iters;         /* saturation iterations (default 10) */
+    int dag_search;        /* 1: DAG-cost local search after greedy (default), 0: greedy only */
+} acs_opt_limits;
+
+/* Optimizes every directive-marked region of `source` for `variant`
+ * ("cse", "cse+sat", "cse+bulk", "accsat").  On success *text_out holds the
+ * emitted module and *json_out a satcc-metrics-v1 document (free both with
+ * acs_opt_free).  Returns 0, or 1 with *json_out = {"error": ...} when the
+ * source does not parse (per-region failures are fail-open: the region is
+ * left untouched and its metrics carry the error). */
+int acs_opt_optimize(const char* source, const char* name, const char* variant, const acs_opt_limits* limits,
+                     char** text_out, char** json_out);
+void acs_opt_free(char* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACCSAT_OPT_H */
