@@ -1,0 +1,167 @@
+// acs-satcc — command-line driver over host stage (a) (include/accsat_opt.h),
+// option-compatible with the reference CLI's core (proj/tools/satcc_main.cpp):
+//
+//   acs-satcc [opt] [--variant V] [-o FILE] file        optimized source
+//   acs-satcc report [--variant V] file...              satcc-metrics-v1 JSON
+//   acs-satcc [--variant V] [--keep] -- cmd args...     wrapper mode: every
+//        existing *.c argument is optimized into <tmp>/<argidx>/<basename> and
+//        cmd runs on the substituted paths; exit code propagated (128+signal,
+//        127 if exec fails); an unparseable file passes through unchanged
+//        (satcc_main.cpp:285-360).
+//
+// Flags: --variant (cse | cse+sat | cse+bulk | accsat, default accsat),
+// --max-nodes, --sat-time, --iters, --extract greedy|dag, --no-sat, --no-bulk.
+#include <sys/stat.h>
+#include <sys/wait.h>
+#include <unistd.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/accsat_opt.h"
+
+static std::string read_file(const std::string& p) {
+    std::ifstream in(p, std::ios::binary);
+    if (!in) throw std::runtime_error("cannot open " + p);
+    std::ostringstream ss;
+    ss << in.rdbuf();
+    return ss.str();
+}
+
+int main(int argc, char** argv) {
+    std::vector<std::string> args(argv + 1, argv + argc);
+    std::string cmd = "opt", variant = "accsat", output;
+    acs_opt_limits lim{10000, 10.0, 10, 1};
+    bool no_sat = false, no_bulk = false, keep = false;
+    std::vector<std::string> files, child;
+    size_t i = 0;
+    if (!args.empty() && (args[0] == "opt" || args[0] == "report")) cmd = args[i++];
+    for (; i < args.size(); ++i) {
+        const std::string& a = args[i];
+        auto next = [&]() -> std::string {
+            if (i + 1 >= args.size()) {
+                std::cerr << "acs-satcc: " << a << " needs a value\n";
+                std::exit(2);
+            }
+            return args[++i];
+        };
+        if (a == "--") {
+            child.assign(args.begin() + (long)i + 1, args.end());
+            cmd = "wrap";
+            break;
+        } else if (a == "--variant") variant = next();
+        else if (a == "-o") output = next();
+        else if (a == "--max-nodes") lim.max_nodes = std::stol(next());
+        else if (a == "--sat-time") lim.max_time_s = std::stod(next());
+        else if (a == "--iters") lim.max_iters = std::stoi(next());
+        else if (a == "--extract") lim.dag_search = next() == "greedy" ? 0 : 1;
+        else if (a == "--no-sat") no_sat = true;
+        else if (a == "--no-bulk") no_bulk = true;
+        else if (a == "--keep") keep = true;
+        else files.push_back(a);
+    }
+    bool sat = variant == "accsat" || variant == "cse+sat", bulk = variant == "accsat" || variant == "cse+bulk";
+    if (no_sat) sat = false;
+    if (no_bulk) bulk = false;
+    std::string v = sat && bulk ? "accsat" : sat ? "cse+sat" : bulk ? "cse+bulk" : "cse";
+
+    auto optimize = [&](const std::string& path, std::string& text, std::string& json) {
+        char *t = nullptr, *j = nullptr;
+        std::string src = read_file(path);
+        int rc = acs_opt_optimize(src.c_str(), path.c_str(), v.c_str(), &lim, &t, &j);
+        text = t;
+        json = j;
+        acs_opt_free(t);
+        acs_opt_free(j);
+        return rc;
+    };
+
+    if (cmd == "wrap") {
+        if (child.empty()) {
+            std::cerr << "acs-satcc: nothing to run after --\n";
+            return 2;
+        }
+        std::string tmp;
+        if (keep) {
+            tmp = "satcc-cache";
+            mkdir(tmp.c_str(), 0755);
+        } else {
+            char tpl[] = "/tmp/acs-satcc-XXXXXX";
+            if (!mkdtemp(tpl)) return 127;
+            tmp = tpl;
+        }
+        for (size_t a = 0; a < child.size(); ++a) {
+            const std::string& f = child[a];
+            if (f.size() < 2 || f.compare(f.size() - 2, 2, ".c") != 0) continue;
+            struct stat st;
+            if (stat(f.c_str(), &st) != 0) continue;
+            std::string text, json;
+            try {
+                if (optimize(f, text, json) != 0) {
+                    std::cerr << "acs-satcc: warning: " << f << " passed through unchanged: " << json << "\n";
+                    continue;
+                }
+            } catch (const std::exception& e) {
+                std::cerr << "acs-satcc: warning: " << f << ": " << e.what() << "\n";
+                continue;
+            }
+            std::string dir = tmp + "/" + std::to_string(a);
+            mkdir(dir.c_str(), 0755);
+            std::string base = f.substr(f.find_last_of('/') == std::string::npos ? 0 : f.find_last_of('/') + 1);
+            std::string out = dir + "/" + base;
+            std::ofstream(out, std::ios::binary) << text;
+            child[a] = out;
+        }
+        std::vector<char*> av;
+        for (auto& s : child) av.push_back(const_cast<char*>(s.c_str()));
+        av.push_back(nullptr);
+        pid_t pid = fork();
+        if (pid == 0) {
+            execvp(av[0], av.data());
+            _exit(127);
+        }
+        int status = 0;
+        waitpid(pid, &status, 0);
+        if (!keep) {
+            std::string rm = "rm -rf '" + tmp + "'";
+            if (std::system(rm.c_str()) != 0) std::cerr << "acs-satcc: could not remove " << tmp << "\n";
+        }
+        if (WIFEXITED(status)) return WEXITSTATUS(status);
+        if (WIFSIGNALED(status)) return 128 + WTERMSIG(status);
+        return 1;
+    }
+
+    if (files.empty()) {
+        std::cerr << "usage: acs-satcc [opt|report] [--variant V] file...  |  acs-satcc [flags] -- cmd args...\n";
+        return 2;
+    }
+    int rc = 0;
+    std::string reports = "[";
+    for (size_t f = 0; f < files.size(); ++f) {
+        std::string text, json;
+        try {
+            int r = optimize(files[f], text, json);
+            if (r) rc = 1;
+        } catch (const std::exception& e) {
+            std::cerr << "acs-satcc: error: " << e.what() << "\n";
+            rc = 1;
+            continue;
+        }
+        if (cmd == "opt") {
+            if (!output.empty())
+                std::ofstream(output, std::ios::binary) << text;
+            else
+                std::cout << text;
+        } else {
+            reports += (f ? ",\n" : "\n") + json;
+        }
+    }
+    if (cmd == "report") std::cout << reports << "]\n";
+    return rc;
+}
