@@ -1,0 +1,96 @@
+"""Host stage (a) on the REFERENCE's own kernel corpus (proj/kernels/*.c,
+read in place — nothing copied): for every kernel and VariantConfig,
+objective_after is never worse than the reference optimizer's (run here
+through oracle/_ref/ref_tool with a 2 s exact-extraction budget), and the
+reference interpreter gives equal results for the original and our emitted
+module on seeded random inputs (doubles U[-10,10], ints U[1,8], the
+distribution of random_env, proj/src/interp.cpp:272-298).  Regions the
+reference leaves untouched or we leave untouched (inner loops: fail-open)
+are compared as such."""
+import glob
+import json
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+import envio
+from paper_2306_13002_b200 import kernel_subset as ks
+from paper_2306_13002_b200 import satopt
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_TOOL = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
+CORPUS = sorted(glob.glob("/root/reference/proj/kernels/*.c"))
+pytestmark = pytest.mark.skipif(not CORPUS or not os.path.exists(REF_TOOL),
+                                reason="needs /root/reference and oracle/_ref/ref_tool")
+
+
+def ref_opt(path, variant):
+    with tempfile.TemporaryDirectory() as td:
+        out, met = os.path.join(td, "o.c"), os.path.join(td, "m.json")
+        r = subprocess.run([REF_TOOL, "opt", variant, path, out, met, "ilp", "2"], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        return open(out).read(), json.load(open(met))
+
+
+def random_env(src, fn_name, seed):
+    mod = ks.parse(src)
+    fn = next(f for f in mod.functions if f.name == fn_name)
+    rng = np.random.default_rng(seed)
+    scalars, arrays = {}, {}
+    decls = [(d[0], g.ty, d[1]) for g in mod.globals for d in g.names] + [(p.name, p.ty, p.dims) for p in fn.params]
+    for name, ty, dims in decls:
+        if dims:
+            n = int(np.prod(dims))
+            arrays[name] = (rng.integers(1, 9, n) if ty == "int" else rng.uniform(-10, 10, n)).reshape(dims)
+        else:
+            scalars[name] = ("int", int(rng.integers(1, 9))) if ty == "int" else ("double", float(rng.uniform(-10, 10)))
+    return scalars, arrays
+
+
+def ref_eval(text, fn, scalars, arrays):
+    with tempfile.TemporaryDirectory() as td:
+        src = os.path.join(td, "k.c")
+        open(src, "w").write(text)
+        ein, eout = os.path.join(td, "in.bin"), os.path.join(td, "out.bin")
+        envio.write_env(ein, scalars, arrays)
+        r = subprocess.run([REF_TOOL, "eval", src, fn, ein, eout], capture_output=True, text=True)
+        return (r.returncode, envio.read_env(eout) if r.returncode == 0 else r.stderr)
+
+
+def close(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    both_nan = np.isnan(a) & np.isnan(b)
+    d = np.abs(a - b)
+    return np.all(both_nan | (d <= 1e-9 * np.maximum(np.abs(a), np.abs(b))) | (d <= 1e-12))
+
+
+@pytest.mark.parametrize("path", CORPUS, ids=[os.path.basename(p) for p in CORPUS])
+@pytest.mark.parametrize("variant", ["cse", "cse+sat", "cse+bulk", "accsat"])
+def test_corpus_kernel(path, variant):
+    src = open(path).read()
+    mine, meta = satopt.optimize_source(src, os.path.basename(path), variant)
+    _, ref = ref_opt(path, variant)
+    assert len(meta["regions"]) == len(ref["regions"])
+    for m, r in zip(meta["regions"], ref["regions"]):
+        assert m["function"] == r["function"]
+        if m["error"] or r["error"]:
+            continue
+        assert m["objective_before"] == r["objective_before"], (m, r)
+        assert m["objective_after"] <= r["objective_after"], (m, r)
+    for fn in {r["function"] for r in meta["regions"]}:
+        for seed in (1, 2):
+            sc, ar = random_env(src, fn, seed)
+            rc0, want = ref_eval(src, fn, sc, ar)
+            rc1, got = ref_eval(mine, fn, sc, ar)
+            assert rc0 == rc1, (rc0, rc1, want if rc0 else got)
+            if rc0:
+                continue
+            for name, v in want[1].items():
+                assert close(got[1][name], v), f"{os.path.basename(path)}:{fn}/{variant}: array {name}"
+            for name, (_, v) in want[0].items():
+                if name.startswith("_"):
+                    continue
+                assert close(got[0][name][1], v), f"{os.path.basename(path)}:{fn}/{variant}: scalar {name}"
