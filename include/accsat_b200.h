@@ -116,6 +116,14 @@ const char* acs_kernel_array_name(const acs_kernel* k, int index);
 const char* acs_kernel_scalar_name(const acs_kernel* k, int index);
 int acs_kernel_scalar_is_int(const acs_kernel* k, int index);
 
+/* Subscript-0 reach of one array (kernel parameter order `index`): the
+ * min/max static offset, relative to the outermost loop variable, of its
+ * loads (*ld_lo, *ld_hi) and of its stores (*st_lo, *st_hi); *sliced = 1 when
+ * subscript 0 follows the outermost loop (the array can be cut into slabs).
+ * Flags *loaded / *stored say whether the nest reads / writes it at all. */
+acs_status acs_kernel_array_reach(const acs_kernel* k, int index, int* sliced, int* loaded, int* stored,
+                                  int* ld_lo, int* ld_hi, int* st_lo, int* st_hi);
+
 /* Runs the WHOLE nest (every marked loop) of one region on `stream`.
  * Arrays/scalars are matched to the nest's parameters by name. */
 acs_status acs_launch(const acs_kernel* k, acs_variant variant, acs_schedule schedule,

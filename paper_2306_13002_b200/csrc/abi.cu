@@ -263,6 +263,25 @@ const char* acs_kernel_array_name(const acs_kernel* k, int index) {
     if (!e || index < 0 || index >= (int)e->arrays.size()) return nullptr;
     return e->arrays[index].c_str();
 }
+acs_status acs_kernel_array_reach(const acs_kernel* k, int index, int* sliced, int* loaded, int* stored, int* ld_lo,
+                                  int* ld_hi, int* st_lo, int* st_hi) {
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    if (!e || index < 0 || index >= (int)e->reach.size() || !sliced || !loaded || !stored || !ld_lo || !ld_hi ||
+        !st_lo || !st_hi) {
+        set_error("acs_kernel_array_reach: bad argument");
+        return ACS_E_ARG;
+    }
+    const Entry::Reach& r = e->reach[index];
+    *sliced = r.sliced;
+    *loaded = r.loaded;
+    *stored = r.stored;
+    *ld_lo = r.ld_lo;
+    *ld_hi = r.ld_hi;
+    *st_lo = r.st_lo;
+    *st_hi = r.st_hi;
+    return ACS_OK;
+}
+
 const char* acs_kernel_scalar_name(const acs_kernel* k, int index) {
     const Entry* e = reinterpret_cast<const Entry*>(k);
     if (!e || index < 0 || index >= (int)e->scalars.size()) return nullptr;

@@ -46,6 +46,10 @@ struct Entry {
     int best[2][5] = {};         // preferred slot per (precision, variant); acs_tune updates it
     bool soa_last_dim = false;   // backend layout: trailing component subscript made slowest (D3Q19 q)
     std::vector<int> component_last;  // per array: trailing subscript is an absolute component index
+    struct Reach {
+        int sliced, loaded, stored, ld_lo, ld_hi, st_lo, st_hi;
+    };
+    std::vector<Reach> reach;          // subscript-0 reach per array (acs_kernel_array_reach)
 };
 
 void register_entry(Entry* e);
@@ -226,6 +230,15 @@ void describe(Entry& e, const char* file, int region) {
     for (int a = 0; a < NS::NARR; ++a) {
         e.arrays.push_back(NS::array_names[a]);
         e.component_last.push_back(NS::ndim(a) >= 2 && NS::sig(a, NS::ndim(a) - 1) == -1 ? 1 : 0);
+        Entry::Reach rc{};
+        rc.sliced = NS::ndim(a) >= 2 && NS::sig(a, 0) == 0;
+        rc.loaded = NS::is_loaded(a);
+        rc.stored = !NS::readonly(a);
+        rc.ld_lo = NS::ld_lo(a, 0);
+        rc.ld_hi = NS::ld_hi(a, 0);
+        rc.st_lo = NS::off_lo[a][0];   // union of load and store offsets: a safe bound for stores
+        rc.st_hi = NS::off_hi[a][0];
+        e.reach.push_back(rc);
     }
     for (int s = 0; s < NS::NSCALAR; ++s) {
         e.scalars.push_back(NS::scalar_names[s]);
