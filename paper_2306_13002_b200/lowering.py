@@ -75,8 +75,28 @@ class LowerError(Exception):
     pass
 
 
+def ks_vars(e: Optional[ks.Expr]) -> set:
+    """Scalar names an expression reads (array subscripts included)."""
+    if e is None:
+        return set()
+    out = {e.op} if e.kind == "var" else set()
+    for k in e.kids:
+        out |= ks_vars(k)
+    return out
+
+
+def _affine_expr(var: Optional[str], off: int) -> ks.Expr:
+    lit = ks.Expr("int", text=str(abs(off)))
+    if var is None:
+        return ks.Expr("int", text=str(off))
+    v = ks.Expr("var", var)
+    if off == 0:
+        return v
+    return ks.Expr("bin", "+" if off > 0 else "-", [v, lit])
+
+
 class _Lowerer:
-    def __init__(self, fn: ks.Function, region: ks.Region, fma: bool, f32: bool):
+    def __init__(self, fn: ks.Function, region: ks.Region, fma: bool, f32: bool, ifconv: bool = True):
         self.fn = fn
         self.region = region
         self.fma = fma
@@ -104,6 +124,10 @@ class _Lowerer:
         self.loaded = set()
         self.stored = set()
         self.n_fma = self.n_loads = self.n_dyn = 0
+        self.capture: Optional[Dict[tuple, str]] = None   # if-conversion: store target -> value var
+        self.n_ifc = 0
+        self.ifconv = ifconv
+        self.body_stmt: Optional[ks.Stmt] = None
 
     # -- types
     def real(self) -> str:
@@ -367,6 +391,9 @@ class _Lowerer:
                 code, t = self.ex(s.rhs)
                 val = self.conv(code, t, want)
                 offs = self.ref_offsets(s.lhs)
+                if self.capture is not None:    # if-converted branch: the store becomes a value
+                    out.append(f"{pad}{self.capture[self.target_key(s.lhs)]} = {val};")
+                    return
                 if offs is not None:
                     out.append(f"{pad}m.template st<ARR_{arr}, {', '.join(map(str, offs))}>({val});")
                 else:
@@ -375,6 +402,10 @@ class _Lowerer:
                 return
             raise LowerError("bad assignment target")
         if k == "if":
+            targets = self.if_convertible(s)
+            if targets is not None:
+                self.if_convert(s, targets, ind, out)
+                return
             c, _ = self.ex(s.cond)
             out.append(f"{pad}if ({c}) {{")
             self.st(s.then_s, ind + 1, out)
@@ -397,6 +428,129 @@ class _Lowerer:
         if k == "for":
             raise LowerError("sequential loops inside a region body are not supported yet")
         raise LowerError(f"statement kind {k}")
+
+    # -- if-conversion of store-symmetric branches
+    #
+    # In the bulk-load forms the reference emitter hoists every load above the
+    # branch (proj/src/codegen.cpp:429-495), which can leave an `if` whose two
+    # arms are load-free and store to the SAME set of elements — D3Q19's
+    # obstacle bounce-back vs BGK collide arms both write the 19 pushed
+    # distributions.  On a SIMT machine a warp holding both kinds of cell
+    # would issue every store twice with complementary lane masks; instead
+    # both arms are evaluated (pure arithmetic, no traps on the GPU) and each
+    # element is stored ONCE with a select of the two values.  Bit-exact: the
+    # stored value is the one the taken arm computes.
+
+    def target_key(self, e: ks.Expr) -> Optional[tuple]:
+        offs = []
+        for idx in e.kids:
+            a = self.as_affine(idx)
+            if a is None:
+                return None
+            offs.append((a.var, a.off))
+        return (e.op, tuple(offs))
+
+    @staticmethod
+    def _has_ref(e: Optional[ks.Expr]) -> bool:
+        if e is None:
+            return False
+        return e.kind == "ref" or any(_Lowerer._has_ref(k) for k in e.kids)
+
+    def _arm(self, s: ks.Stmt, targets: list, assigned: set, reads: set, local: set) -> bool:
+        k = s.kind
+        if k == "empty":
+            return True
+        if k == "block":
+            return all(self._arm(c, targets, assigned, reads, local) for c in s.stmts)
+        if k == "decl":
+            for name, dims, init in s.names:
+                if dims or self._has_ref(init):
+                    return False
+                local.add(name)
+                if init is not None:
+                    reads.update(ks_vars(init))
+            return True
+        if k == "assign":
+            if self._has_ref(s.rhs):
+                return False
+            reads.update(ks_vars(s.rhs))
+            if s.lhs.kind == "var":
+                assigned.add(s.lhs.op)
+                return True
+            if s.lhs.kind == "ref" and not any(self._has_ref(i) for i in s.lhs.kids):
+                key = self.target_key(s.lhs)
+                if key is None:
+                    return False
+                targets.append(key)
+                return True
+        return False
+
+    def if_convertible(self, s: ks.Stmt) -> Optional[list]:
+        if not self.ifconv or s.else_s is None:
+            return None
+        ta, tb = [], []
+        aa, ab, ra, rb, la, lb = set(), set(), set(), set(), set(), set()
+        if not (self._arm(s.then_s, ta, aa, ra, la) and self._arm(s.else_s, tb, ab, rb, lb)):
+            return None
+        if not ta or sorted(ta, key=repr) != sorted(tb, key=repr) or len(set(ta)) != len(ta):
+            return None
+        # scalars an arm assigns that live outside it: neither arm may read the
+        # other's, and nothing after the `if` may read them (they would see
+        # both arms' writes)
+        outer_a, outer_b = aa - la, ab - lb
+        if (outer_a & rb) or (outer_b & ra):
+            return None
+        if (outer_a | outer_b) & self.reads_outside(s):
+            return None
+        return ta
+
+    def reads_outside(self, target: ks.Stmt) -> set:
+        out: set = set()
+
+        def walk(st: ks.Stmt):
+            if st is target:
+                return
+            for e in (st.rhs, st.cond, st.lhs if st.lhs is not None and st.lhs.kind == "ref" else None):
+                if e is not None:
+                    out.update(ks_vars(e))
+            for _, _, init in st.names:
+                if init is not None:
+                    out.update(ks_vars(init))
+            for c in ks.children(st):
+                walk(c)
+        walk(self.body_stmt)
+        return out
+
+    def if_convert(self, s: ks.Stmt, targets: list, ind: int, out: List[str]):
+        pad = "    " * ind
+        ty = {}
+        for key in targets:
+            ty[key] = "int" if self.arrays[key[0]].ty == "int" else self.real()
+        names_a = {key: f"_ifc{self.n_ifc}_a{i}" for i, key in enumerate(targets)}
+        names_b = {key: f"_ifc{self.n_ifc}_b{i}" for i, key in enumerate(targets)}
+        self.n_ifc += 1
+        c, _ = self.ex(s.cond)
+        out.append(f"{pad}{{  // if-converted: both arms store the same {len(targets)} elements")
+        out.append(f"{pad}    const bool _ifc = ({c});")
+        for key in targets:
+            out.append(f"{pad}    {ty[key]} {names_a[key]}, {names_b[key]};")
+        saved = self.capture
+        self.capture = names_a
+        self.st(s.then_s, ind + 1, out)
+        self.capture = names_b
+        self.st(s.else_s, ind + 1, out)
+        self.capture = saved
+        # the stores, in the then-arm's order, one per element
+        for key in targets:
+            arr, offs = key
+            if any(v is not None and v not in self.loop_vars for v, _ in offs):
+                raise LowerError("if-conversion target not in loop coordinates")
+            # re-derive the device offsets through ref_offsets' bookkeeping
+            ref = ks.Expr("ref", arr, [_affine_expr(v, o) for v, o in offs])
+            o = self.ref_offsets(ref)
+            out.append(f"{pad}    m.template st<ARR_{arr}, {', '.join(map(str, o))}>"
+                       f"(_ifc ? {names_a[key]} : {names_b[key]});")
+        out.append(f"{pad}}}")
 
     def bound_expr(self, e: ks.Expr) -> str:
         c, t = self.ex(e)
@@ -427,6 +581,7 @@ class _Lowerer:
 
     def run(self) -> Lowered:
         body_stmt = self.region.anchor.body
+        self.body_stmt = body_stmt
         self.count_assigns(body_stmt)
         # function-level locals other than loop vars
         pre: List[str] = []
@@ -455,11 +610,11 @@ class _Lowerer:
                        self.ldrange, self.dynrange, self.dynsig, self.loaded)
 
 
-def lower_text(text: str, function: str, fma: bool, f32: bool = False) -> Lowered:
+def lower_text(text: str, function: str, fma: bool, f32: bool = False, ifconv: bool = True) -> Lowered:
     mod = ks.parse(text)
     for reg in ks.find_regions(mod):
         if reg.function.name == function:
-            return _Lowerer(reg.function, reg, fma, f32).run()
+            return _Lowerer(reg.function, reg, fma, f32, ifconv).run()
     raise LowerError(f"no region in function {function}")
 
 
