@@ -124,6 +124,34 @@ int acs_kernel_scalar_is_int(const acs_kernel* k, int index);
 acs_status acs_kernel_array_reach(const acs_kernel* k, int index, int* sliced, int* loaded, int* stored,
                                   int* ld_lo, int* ld_hi, int* st_lo, int* st_hi);
 
+/* Unconditional static store targets of array `index`: the elements the nest
+ * writes at EVERY point of its iteration space on every path (a store in
+ * both arms of an if counts; the intersection over all five forms).  Target i
+ * is offsets[i*ACS_MAX_DIMS + p]: for a subscript that follows a loop variable
+ * the constant offset from it, for an absolute subscript the constant;
+ * loop_of[p] (optional, ACS_MAX_DIMS entries) = that loop's index, or -1.  Lets a
+ * host-buffer caller skip uploading elements the launch overwrites (the
+ * eval_region contract, proj/src/interp.cpp:266-270, returns every element:
+ * unwritten ones keep their input value).  *n_targets = total count; at most
+ * max_targets are written. */
+acs_status acs_kernel_must_write(const acs_kernel* k, int index, int32_t* loop_of, int max_targets,
+                                 int32_t* offsets, int* n_targets);
+
+/* Iteration space of the marked loops (n_loops entries, outermost first,
+ * half-open [lo, hi)) that acs_launch would run for these scalars — the
+ * parsed init/for_cond of each For (proj/include/satcc/ast.hpp:114-118). */
+acs_status acs_kernel_iteration_space(const acs_kernel* k, const acs_scalar* scalars, int n_scalars, int64_t* lo,
+                                      int64_t* hi);
+
+/* Copies the box [box_lo, box_hi) of a row-major array (identical dims on both
+ * sides) between host and device memory: kind 0 = host->device, 1 =
+ * device->host, 2 = device->device, 3 = inferred (unified addressing).
+ * Asynchronous on `cuda_stream` (pinned host memory for overlap); trailing
+ * full positions are fused into one contiguous run, three positions per
+ * DMA descriptor (cudaMemcpy3DAsync). */
+acs_status acs_copy_box(void* dst, const void* src, int elem_size, int ndim, const int64_t* dims,
+                        const int64_t* box_lo, const int64_t* box_hi, int kind, void* cuda_stream);
+
 /* Runs the WHOLE nest (every marked loop) of one region on `stream`.
  * Arrays/scalars are matched to the nest's parameters by name. */
 acs_status acs_launch(const acs_kernel* k, acs_variant variant, acs_schedule schedule,

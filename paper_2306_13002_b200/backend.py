@@ -20,7 +20,7 @@ from __future__ import annotations
 import ctypes
 import os
 from dataclasses import dataclass, field
-from typing import Dict, Optional, Tuple
+from typing import Dict, List, Optional, Tuple
 
 import numpy as np
 
@@ -207,6 +207,28 @@ class Kernel:
                               _stream_handle(stream), reps, ctypes.byref(best), ms), f"acs_tune({self.kernel_id})")
         return best.value, {i: ms[i] for i in range(8) if ms[i] >= 0}
 
+    def iteration_space(self, scalars: Dict[str, float]) -> List[Tuple[int, int]]:
+        """[lo, hi) of every marked loop (outermost first) for these scalars."""
+        _, sc = self._pack({}, scalars)
+        n = self.info["n_loops"]
+        lo, hi = (ctypes.c_int64 * 8)(), (ctypes.c_int64 * 8)()
+        f = lib().acs_kernel_iteration_space
+        f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+        _check(f(self.handle, sc, len(scalars), lo, hi), "acs_kernel_iteration_space")
+        return [(lo[d], hi[d]) for d in range(n)]
+
+    def must_write(self, name: str) -> Tuple[List[int], List[Tuple[int, ...]]]:
+        """(loop index or -1 per subscript position, unconditional store targets)."""
+        idx = self.info["arrays"].index(name)
+        loop_of = (ctypes.c_int32 * 8)()
+        n = ctypes.c_int()
+        f = lib().acs_kernel_must_write
+        f.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+        _check(f(self.handle, idx, loop_of, 0, None, ctypes.byref(n)), "acs_kernel_must_write")
+        offs = (ctypes.c_int32 * (8 * max(1, n.value)))()
+        _check(f(self.handle, idx, loop_of, n.value, offs, ctypes.byref(n)), "acs_kernel_must_write")
+        return list(loop_of), [tuple(offs[i * 8:(i + 1) * 8]) for i in range(n.value)]
+
     def native_strides(self, name: str, dims: Tuple[int, ...]) -> Tuple[int, ...]:
         d = (ctypes.c_int64 * len(dims))(*dims)
         s = (ctypes.c_int64 * len(dims))()
@@ -221,6 +243,22 @@ def fill(t, kind: str, seed: int, lo: float = 0.0, hi: float = 1.0, p: float = 0
     a = describe("fill", t)
     _check(lib().acs_fill(ctypes.byref(a), FILL[kind], seed, lo, hi, p, flat_offset, _stream_handle(stream)),
            "acs_fill")
+
+
+def copy_box(dst, src, lo, hi, stream=None) -> None:
+    """acs_copy_box: box [lo, hi) of two row-major tensors with equal shapes
+    (host<->device, async on `stream`; pinned host memory overlaps)."""
+    assert tuple(dst.shape) == tuple(src.shape) and dst.dtype == src.dtype
+    assert dst.is_contiguous() and src.is_contiguous()
+    nd = dst.dim()
+    kind = {(False, True): 0, (True, False): 1, (True, True): 2}.get((src.is_cuda, dst.is_cuda), 3)
+    f = lib().acs_copy_box
+    f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                  ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    dims = (ctypes.c_int64 * nd)(*dst.shape)
+    l, h = (ctypes.c_int64 * nd)(*lo), (ctypes.c_int64 * nd)(*hi)
+    _check(f(dst.data_ptr(), src.data_ptr(), dst.element_size(), nd, dims, l, h, kind, _stream_handle(stream)),
+           "acs_copy_box")
 
 
 def copy(dst, src, stream=None) -> None:

@@ -282,6 +282,95 @@ acs_status acs_kernel_array_reach(const acs_kernel* k, int index, int* sliced, i
     return ACS_OK;
 }
 
+acs_status acs_kernel_must_write(const acs_kernel* k, int index, int32_t* loop_of, int max_targets, int32_t* offsets,
+                                 int* n_targets) {
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    if (!e || index < 0 || index >= (int)e->must_write.size() || !n_targets || max_targets < 0 ||
+        (max_targets > 0 && !offsets)) {
+        set_error("acs_kernel_must_write: bad argument");
+        return ACS_E_ARG;
+    }
+    if (loop_of)
+        for (int p = 0; p < ACS_MAX_DIMS; ++p) loop_of[p] = e->loop_of[index][p];
+    const auto& t = e->must_write[index];
+    *n_targets = (int)t.size();
+    for (int i = 0; i < (int)t.size() && i < max_targets; ++i)
+        for (int p = 0; p < ACS_MAX_DIMS; ++p) offsets[i * ACS_MAX_DIMS + p] = t[i][p];
+    return ACS_OK;
+}
+
+acs_status acs_kernel_iteration_space(const acs_kernel* k, const acs_scalar* scalars, int n_scalars, int64_t* lo,
+                                      int64_t* hi) {
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    if (!e || !e->space || (n_scalars > 0 && !scalars) || !lo || !hi) {
+        set_error("acs_kernel_iteration_space: bad argument");
+        return ACS_E_ARG;
+    }
+    long long l[ACS_MAX_DIMS], h[ACS_MAX_DIMS];
+    const acs_status st = e->space(scalars, n_scalars, l, h);
+    if (st != ACS_OK) return st;
+    for (int d = 0; d < e->n_loops; ++d) {
+        lo[d] = l[d];
+        hi[d] = h[d];
+    }
+    return ACS_OK;
+}
+
+acs_status acs_copy_box(void* dst, const void* src, int elem_size, int ndim, const int64_t* dims,
+                        const int64_t* box_lo, const int64_t* box_hi, int kind, void* cuda_stream) {
+    if (!dst || !src || elem_size <= 0 || ndim < 1 || ndim > ACS_MAX_DIMS || !dims || !box_lo || !box_hi ||
+        kind < 0 || kind > 3) {
+        set_error("acs_copy_box: bad argument");
+        return ACS_E_ARG;
+    }
+    for (int p = 0; p < ndim; ++p) {
+        if (dims[p] < 0 || box_lo[p] < 0 || box_hi[p] > dims[p]) {
+            set_error("acs_copy_box: box outside the array");
+            return ACS_E_BOUNDS;
+        }
+        if (box_hi[p] <= box_lo[p]) return ACS_OK;   // empty box
+    }
+    // innermost position k whose inner positions are all full: one contiguous run
+    int k = ndim - 1;
+    while (k > 0 && box_lo[k] == 0 && box_hi[k] == dims[k]) --k;
+    size_t inner = (size_t)elem_size;   // bytes of one index step at position k
+    for (int p = k + 1; p < ndim; ++p) inner *= (size_t)dims[p];
+    const size_t width = inner * (size_t)(box_hi[k] - box_lo[k]);
+    const size_t pitch = inner * (size_t)dims[k];
+    const int64_t h_dim = k >= 1 ? dims[k - 1] : 1;
+    const int64_t h_lo = k >= 1 ? box_lo[k - 1] : 0, h_n = k >= 1 ? box_hi[k - 1] - box_lo[k - 1] : 1;
+    const int64_t d_lo = k >= 2 ? box_lo[k - 2] : 0, d_n = k >= 2 ? box_hi[k - 2] - box_lo[k - 2] : 1;
+    const size_t slice = pitch * (size_t)h_dim;
+    const size_t block = k >= 2 ? slice * (size_t)dims[k - 2] : slice;   // bytes of one step at position k-3
+    static const cudaMemcpyKind kinds[4] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost,
+                                            cudaMemcpyDeviceToDevice, cudaMemcpyDefault};
+    // positions outside k-2 are iterated here (row-major offset of the outer index)
+    int64_t outer_n = 1;
+    for (int p = 0; p < k - 2; ++p) outer_n *= box_hi[p] - box_lo[p];
+    for (int64_t o = 0; o < outer_n; ++o) {
+        size_t off = 0, rem = (size_t)o, mul = block;
+        for (int p = k - 3; p >= 0; --p) {
+            const int64_t n = box_hi[p] - box_lo[p];
+            off += (size_t)(box_lo[p] + (int64_t)(rem % (size_t)n)) * mul;
+            rem /= (size_t)n;
+            mul *= (size_t)dims[p];
+        }
+        const size_t base = off + (size_t)d_lo * slice + (size_t)h_lo * pitch + (size_t)box_lo[k] * inner;
+        cudaMemcpy3DParms prm = {};
+        prm.srcPtr = make_cudaPitchedPtr(const_cast<char*>(static_cast<const char*>(src)) + base, pitch, width,
+                                         (size_t)h_dim);
+        prm.dstPtr = make_cudaPitchedPtr(static_cast<char*>(dst) + base, pitch, width, (size_t)h_dim);
+        prm.extent = make_cudaExtent(width, (size_t)h_n, (size_t)d_n);
+        prm.kind = kinds[kind];
+        cudaError_t err = cudaMemcpy3DAsync(&prm, static_cast<cudaStream_t>(cuda_stream));
+        if (err != cudaSuccess) {
+            set_error(std::string("acs_copy_box: ") + cudaGetErrorString(err));
+            return ACS_E_CUDA;
+        }
+    }
+    return ACS_OK;
+}
+
 const char* acs_kernel_scalar_name(const acs_kernel* k, int index) {
     const Entry* e = reinterpret_cast<const Entry*>(k);
     if (!e || index < 0 || index >= (int)e->scalars.size()) return nullptr;

@@ -4,6 +4,8 @@
 // generated nest struct (csrc/gen/<nest>.cuh).
 #pragma once
 
+#include <array>
+
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -50,6 +52,12 @@ struct Entry {
         int sliced, loaded, stored, ld_lo, ld_hi, st_lo, st_hi;
     };
     std::vector<Reach> reach;          // subscript-0 reach per array (acs_kernel_array_reach)
+    // per array: unconditional static store targets of every form, one offset
+    // (loop-mapped position) or constant (absolute position) per subscript
+    std::vector<std::vector<std::array<int, 8>>> must_write;
+    std::vector<std::array<int, 8>> loop_of;   // per array/position: loop index (NS::sig) or -1
+    // iteration space of the marked loops for these scalars (half-open)
+    acs_status (*space)(const acs_scalar* sc, int n, long long* lo, long long* hi) = nullptr;
 };
 
 void register_entry(Entry* e);
@@ -224,7 +232,25 @@ void fill_naive_occ(Entry& e, int prec) {
 }
 
 template <class NS>
+acs_status eval_space(const acs_scalar* sc, int n, long long* lo, long long* hi) {
+    typename NS::Scalars s{};
+    for (int i = 0; i < NS::NSCALAR; ++i) {
+        const acs_scalar* d = nullptr;
+        for (int j = 0; j < n; ++j)
+            if (sc[j].name && std::strcmp(sc[j].name, NS::scalar_names[i]) == 0) d = &sc[j];
+        if (!d) {
+            set_error(std::string("missing scalar argument '") + NS::scalar_names[i] + "'");
+            return ACS_E_ARG;
+        }
+        NS::set_scalar(s, i, d->is_int ? d->i : (long long)d->d, d->is_int ? (double)d->i : d->d);
+    }
+    NS::bounds(s, lo, hi);
+    return ACS_OK;
+}
+
+template <class NS>
 void describe(Entry& e, const char* file, int region) {
+    e.space = &eval_space<NS>;
     e.region = region;
     e.n_loops = NS::NLOOP;
     for (int a = 0; a < NS::NARR; ++a) {
@@ -239,6 +265,16 @@ void describe(Entry& e, const char* file, int region) {
         rc.st_lo = NS::off_lo[a][0];   // union of load and store offsets: a safe bound for stores
         rc.st_hi = NS::off_hi[a][0];
         e.reach.push_back(rc);
+        std::array<int, 8> lo_of{};
+        for (int p = 0; p < 8; ++p) lo_of[p] = p < NS::ndim(a) ? NS::sig(a, p) : -1;
+        e.loop_of.push_back(lo_of);
+        e.must_write.emplace_back();
+        for (int t = 0; t < NS::n_must_write; ++t)
+            if (NS::must_write_arr[t] == a) {
+                std::array<int, 8> o{};
+                for (int p = 0; p < 8; ++p) o[p] = NS::must_write_off[t][p];
+                e.must_write.back().push_back(o);
+            }
     }
     for (int s = 0; s < NS::NSCALAR; ++s) {
         e.scalars.push_back(NS::scalar_names[s]);

@@ -69,6 +69,9 @@ class Lowered:
     dynrange: Dict[str, list] = field(default_factory=dict)
     dynsig: Dict[str, List[int]] = field(default_factory=dict)
     loaded: set = field(default_factory=set)
+    # unconditional static stores: (array, per-position offset) written at
+    # EVERY point of the iteration space on every path (both arms of an if)
+    must_write: set = field(default_factory=set)
 
 
 class LowerError(Exception):
@@ -552,6 +555,33 @@ class _Lowerer:
                        f"(_ifc ? {names_a[key]} : {names_b[key]});")
         out.append(f"{pad}}}")
 
+    def must_write(self, s: ks.Stmt) -> set:
+        """Store targets executed on every path through `s` (static offsets
+        only; a loop var position gives its offset, an absolute position its
+        constant).  Evaluated after emission, so int temps are resolved."""
+        k = s.kind
+        if k == "block":
+            out = set()
+            for c in s.stmts:
+                out |= self.must_write(c)
+            return out
+        if k == "if":
+            if s.else_s is None:
+                return set()
+            return self.must_write(s.then_s) & self.must_write(s.else_s)
+        if k == "assign" and s.lhs.kind == "ref":
+            key = self.target_key(s.lhs)
+            if key is None:
+                return set()
+            sig = self.sig.get(key[0])
+            offs = tuple(o for _, o in key[1])
+            vars_ = [v for v, _ in key[1]]
+            want = [self.loop_vars[i] if i is not None and i >= 0 else None for i in (sig or [])]
+            if sig is None or vars_ != want:
+                return set()
+            return {(key[0], offs)}
+        return set()
+
     def bound_expr(self, e: ks.Expr) -> str:
         c, t = self.ex(e)
         if t != "int":
@@ -603,11 +633,12 @@ class _Lowerer:
         bounds = self.loop_bounds()
         out: List[str] = list(pre)
         self.st(body_stmt, 1, out)
+        must = self.must_write(body_stmt)
         sig = {a: self.sig.get(a) for a in self.arrays}
         return Lowered(self.fn.name, self.fn.params, self.loop_vars, bounds,
                        {a: (s if s is not None else [-1] * len(self.arrays[a].dims)) for a, s in sig.items()},
                        self.stored, "\n".join(out), self.n_fma, self.n_loads, self.n_dyn, self.offrange,
-                       self.ldrange, self.dynrange, self.dynsig, self.loaded)
+                       self.ldrange, self.dynrange, self.dynsig, self.loaded, must)
 
 
 def lower_text(text: str, function: str, fma: bool, f32: bool = False, ifconv: bool = True) -> Lowered:
@@ -775,6 +806,15 @@ def gen_function(nest: str, function: str, f32: bool = False) -> Tuple[str, dict
              + ", ".join(row(stage[a.name][2]) for a in arrays) + "}; return t[a][p]; }")
     L.append("static __host__ __device__ constexpr int ld_hi(int a, int p) { constexpr int t[NARR][8] = {"
              + ", ".join(row(stage[a.name][3]) for a in arrays) + "}; return t[a][p]; }")
+    must = set.intersection(*(l.must_write for l in lows.values()))
+    names = [a.name for a in arrays]
+    must = sorted(must, key=lambda t: (names.index(t[0]), t[1]))
+    L.append("// unconditional static stores of EVERY form (array, offsets): written at every point")
+    L.append(f"static constexpr int n_must_write = {len(must)};")
+    L.append("static constexpr int must_write_arr[" + str(max(1, len(must))) + "] = {"
+             + (", ".join(f"ARR_{a}" for a, _ in must) if must else "-1") + "};")
+    L.append("static constexpr int must_write_off[" + str(max(1, len(must))) + "][8] = {"
+             + (", ".join(row(list(o)) for _, o in must) if must else row([])) + "};")
     L.append("static constexpr bool has_dynamic_index = " + ("true" if any(m_["dyn_loads"] for m_ in meta.values()) else "false") + ";")
     args = ", ".join(f"pt[{d}]" for d in range(len(base.loop_vars)))
     L.append("template <int FORM, class M>")

@@ -11,16 +11,24 @@ Which planes a chunk needs comes from the kernel's subscript-0 reach
 (``acs_kernel_array_reach``): loaded arrays contribute [p0+ld_lo, p1+ld_hi),
 stored arrays [p0+st_lo, p1+st_hi) (uploaded so elements the nest does not
 write keep their host values); a stored plane is downloaded once no later
-chunk can write it.  Every plane crosses PCIe exactly once per direction, so
+chunk can write it.  Every plane crosses PCIe at most once per direction, so
 the call approaches max(H2D bytes, D2H bytes) / link bandwidth instead of
-their sum plus the compute.  Numerics are those of one whole-range launch
+their sum plus the compute.
+
+A stored array the nest never loads is uploaded only OUTSIDE its write core:
+the box every launch overwrites whatever the inputs are, derived from the
+kernel's unconditional store targets (``acs_kernel_must_write``) and the
+iteration space (``acs_kernel_iteration_space``).  Only the shell around the
+core keeps host values (D3Q19 ``dst``: 120 MB of 2.6 GB), copied as a few
+strided DMA boxes (``acs_copy_box``).  Numerics are those of one whole-range launch
 (each chunk is the same kernel over a sub-range of the outermost loop).
 """
 from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass
-from typing import Dict, List
+import itertools
+from typing import Dict, List, Optional, Tuple
 
 from . import backend
 
@@ -49,6 +57,58 @@ def reaches(k: backend.Kernel) -> Dict[str, Reach]:
     return out
 
 
+def write_core(k: backend.Kernel, name: str, dims, scalars) -> Optional[List[Tuple[int, int]]]:
+    """Box [lo, hi) per position that the launch overwrites for ANY input:
+    every component combination of the absolute subscripts has a target, and
+    the loop-mapped positions take the intersection of the shifted
+    iteration ranges.  None when there is no such box."""
+    loop_of, targets = k.must_write(name)
+    nd = len(dims)
+    space = k.iteration_space(scalars)
+    if not targets or any(h <= l for l, h in space):
+        return None
+    lpos = [p for p in range(nd) if loop_of[p] >= 0]
+    apos = [p for p in range(nd) if loop_of[p] < 0]
+    if len({loop_of[p] for p in lpos}) != len(lpos):
+        return None                                   # one loop in two positions: not a box
+    combos = 1
+    for p in apos:
+        combos *= dims[p]
+    if combos > 4096:
+        return None
+    by_combo: Dict[tuple, tuple] = {}
+    for t in targets:
+        by_combo.setdefault(tuple(t[p] for p in apos), t)
+    core = [[0, dims[p]] for p in range(nd)]
+    for c in itertools.product(*[range(dims[p]) for p in apos]):
+        t = by_combo.get(tuple(c))
+        if t is None:
+            return None
+        for p in lpos:
+            lo, hi = space[loop_of[p]]
+            core[p][0] = max(core[p][0], lo + t[p])
+            core[p][1] = min(core[p][1], hi + t[p])
+    core = [(max(0, l), min(dims[p], h)) for p, (l, h) in enumerate(core)]
+    if any(h <= l for l, h in core):
+        return None
+    return core
+
+
+def shell_boxes(dims, core) -> List[Tuple[List[int], List[int]]]:
+    """The full array minus the core box, as disjoint boxes: for position p,
+    positions < p inside the core, p below or above it, positions > p full."""
+    out = []
+    nd = len(dims)
+    for p in range(nd):
+        for lo_p, hi_p in ((0, core[p][0]), (core[p][1], dims[p])):
+            if hi_p <= lo_p:
+                continue
+            lo = [core[q][0] for q in range(p)] + [lo_p] + [0] * (nd - p - 1)
+            hi = [core[q][1] for q in range(p)] + [hi_p] + list(dims[p + 1:])
+            out.append((lo, hi))
+    return out
+
+
 class HostRunner:
     """Reusable device buffers + streams for repeated host-buffer calls of one
     kernel on one problem shape."""
@@ -65,25 +125,46 @@ class HostRunner:
         self.nat = {n: backend.empty_native(k, n, tuple(t.shape), t.dtype) for n, t in host.items()}
         self.s_h2d, self.s_cmp, self.s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
         self.launches = 0
+        self.shell: Dict[str, List] = {}      # store-only arrays: boxes outside the write core
+        self._shell_key = None
 
-    def _copy_planes(self, name, lo, hi, to_device, stream):
-        """H2D (+ remap into the native layout) or (remap +) D2H of planes [lo, hi)."""
-        t = self.host[name]
-        lo, hi = max(lo, 0), min(hi, t.shape[0])
-        if hi <= lo:
+    def _plan_shells(self, scalars):
+        key = tuple(sorted((n, float(v)) for n, v in scalars.items()))
+        if key == self._shell_key:
             return
-        torch = self.torch
-        with torch.cuda.stream(stream):
-            if to_device:
-                self.rm[name][lo:hi].copy_(t[lo:hi], non_blocking=True)
-                backend.copy(self.nat[name][lo:hi], self.rm[name][lo:hi], stream)
+        self._shell_key = key
+        self.shell = {}
+        for name, r in self.reach.items():
+            if r.sliced and r.stored and not r.loaded:
+                dims = tuple(self.host[name].shape)
+                core = write_core(self.k, name, dims, scalars)
+                if core is not None:
+                    self.shell[name] = shell_boxes(dims, core)
+
+    def _h2d(self, name, lo, hi, stream):
+        """Pinned host -> device staging (reference layout) of planes [lo, hi):
+        copy engine only, so the H2D stream never waits on a kernel."""
+        t = self.host[name]
+        with self.torch.cuda.stream(stream):
+            if name in self.shell:
+                # only the part of planes [lo, hi) outside the write core
+                for blo, bhi in self.shell[name]:
+                    l0, h0 = max(blo[0], lo), min(bhi[0], hi)
+                    if h0 > l0:
+                        backend.copy_box(self.rm[name], t, [l0] + blo[1:], [h0] + bhi[1:], stream)
             else:
-                backend.copy(self.rm[name][lo:hi], self.nat[name][lo:hi], stream)
-                t[lo:hi].copy_(self.rm[name][lo:hi], non_blocking=True)
+                self.rm[name][lo:hi].copy_(t[lo:hi], non_blocking=True)
         self.launches += 1
 
+    @staticmethod
+    def _clip(lo, hi, n):
+        return max(lo, 0), min(hi, n)
+
     def run(self, scalars: Dict[str, float], variant: str = "accsat", schedule="default") -> None:
+        """Three streams: H2D (copy engine) | remap-in + kernel + remap-out |
+        D2H (copy engine), chained per chunk by events."""
         torch = self.torch
+        self._plan_shells(scalars)
         beg, end = self.rp
         b, e = int(scalars[beg]), int(scalars[end])
         n = e - b
@@ -92,20 +173,16 @@ class HostRunner:
         for s in (self.s_h2d, self.s_cmp, self.s_d2h):
             s.wait_stream(cur)
         # whole (non-sliced) arrays once
+        whole = [name for name, r in self.reach.items() if not r.sliced and (r.loaded or r.stored)]
         with torch.cuda.stream(self.s_h2d):
-            for name, r in self.reach.items():
-                if not r.sliced and (r.loaded or r.stored):
-                    self.rm[name].copy_(self.host[name], non_blocking=True)
-                    backend.copy(self.nat[name], self.rm[name], self.s_h2d)
-        uploaded = {n: -10**9 for n in self.host}        # highest plane uploaded so far (exclusive)
-        downloaded = {n: -10**9 for n in self.host}
-        for name, r in self.reach.items():
-            if r.sliced:
-                uploaded[name] = 0 if not (r.loaded or r.stored) else -10**9
-        h2d_done: List = []
-        cmp_done: List = []
+            for name in whole:
+                self.rm[name].copy_(self.host[name], non_blocking=True)
+        uploaded = {nm: -10**9 for nm in self.host}       # highest plane uploaded so far (exclusive)
+        downloaded = {nm: -10**9 for nm in self.host}
+        first = True
         for c in range(self.chunks):
             p0, p1 = cuts[c], cuts[c + 1]
+            remap_in = []
             for name, r in self.reach.items():
                 if not r.sliced or not (r.loaded or r.stored):
                     continue
@@ -116,38 +193,48 @@ class HostRunner:
                 if c == self.chunks - 1:
                     hi = max(hi, self.host[name].shape[0])
                 lo = max(lo, uploaded[name])
-                self._copy_planes(name, lo, hi, True, self.s_h2d)
+                lo, hi = self._clip(lo, hi, self.host[name].shape[0])
+                if hi > lo:
+                    self._h2d(name, lo, hi, self.s_h2d)
+                    remap_in.append((name, lo, hi))
                 uploaded[name] = max(uploaded[name], hi)
             ev = torch.cuda.Event()
             ev.record(self.s_h2d)
-            h2d_done.append(ev)
             self.s_cmp.wait_event(ev)
+            if first:
+                for name in whole:
+                    backend.copy(self.nat[name], self.rm[name], self.s_cmp)
+                first = False
+            for name, lo, hi in remap_in:
+                backend.copy(self.nat[name][lo:hi], self.rm[name][lo:hi], self.s_cmp)
             sc = dict(scalars)
             sc[beg], sc[end] = p0, p1
             self.k.launch(self.nat, sc, variant, schedule, self.s_cmp)
             self.launches += 1
-            ev2 = torch.cuda.Event()
-            ev2.record(self.s_cmp)
-            cmp_done.append(ev2)
-            # planes no later chunk writes are final
-            self.s_d2h.wait_event(ev2)
+            # planes no later chunk writes are final: remap out, then D2H
+            out = []
             for name, r in self.reach.items():
                 if not (r.sliced and r.stored):
                     continue
-                if c + 1 < self.chunks:
-                    final_hi = cuts[c + 1] + r.st_lo
-                else:
-                    final_hi = self.host[name].shape[0]
-                lo = max(downloaded[name], 0 if c == 0 else downloaded[name])
-                lo = 0 if c == 0 else lo
-                self._copy_planes(name, lo, final_hi, False, self.s_d2h)
+                final_hi = cuts[c + 1] + r.st_lo if c + 1 < self.chunks else self.host[name].shape[0]
+                lo = 0 if c == 0 else downloaded[name]
+                lo, hi = self._clip(lo, final_hi, self.host[name].shape[0])
+                if hi > lo:
+                    backend.copy(self.rm[name][lo:hi], self.nat[name][lo:hi], self.s_cmp)
+                    out.append((name, lo, hi))
                 downloaded[name] = max(downloaded[name], final_hi)
-        # non-sliced stored arrays come back whole
-        with torch.cuda.stream(self.s_d2h):
-            for name, r in self.reach.items():
-                if not r.sliced and r.stored:
-                    backend.copy(self.rm[name], self.nat[name], self.s_d2h)
-                    self.host[name].copy_(self.rm[name], non_blocking=True)
+            if c == self.chunks - 1:
+                for name, r in self.reach.items():
+                    if not r.sliced and r.stored:
+                        backend.copy(self.rm[name], self.nat[name], self.s_cmp)
+                        out.append((name, 0, self.host[name].shape[0]))
+            ev2 = torch.cuda.Event()
+            ev2.record(self.s_cmp)
+            self.s_d2h.wait_event(ev2)
+            with torch.cuda.stream(self.s_d2h):
+                for name, lo, hi in out:
+                    self.host[name][lo:hi].copy_(self.rm[name][lo:hi], non_blocking=True)
+                    self.launches += 1
         cur.wait_stream(self.s_d2h)
 
     def bytes_per_call(self):
@@ -155,7 +242,14 @@ class HostRunner:
         for name, r in self.reach.items():
             t = self.host[name]
             nb = t.numel() * t.element_size()
-            if r.loaded or r.stored:
+            if name in self.shell:
+                es = t.element_size()
+                for lo, hi in self.shell[name]:
+                    n = 1
+                    for a, b in zip(lo, hi):
+                        n *= b - a
+                    h2d += n * es
+            elif r.loaded or r.stored:
                 h2d += nb
             if r.stored:
                 d2h += nb

@@ -237,7 +237,22 @@ def test_host_runner_overlapped_equals_oracle(kid, size, dtype, chunks):
     host = {n: torch.from_numpy(a.copy()).pin_memory() for n, a in ins.items()}
     k = backend.Kernel.lookup(kid)
     r = pipeline_exec.HostRunner(k, host, spec.range_params, chunks=chunks)
+    # poison the device staging: elements the shell-only upload skips must be
+    # overwritten by the launch, never read
+    for n in ins:
+        for t in (r.rm[n], r.nat[n]):
+            t.fill_(float("nan") if t.dtype.is_floating_point else -12345)
     r.run(dict(w.scalars), "accsat")
     torch.cuda.synchronize()
     for n in ins:
         assert bitwise_equal(host[n].numpy(), want[n]), f"{kid} chunks={chunks}: '{n}'"
+    # a second call on fresh inputs reuses the buffers and the shell plan
+    ins2 = {n: (a * a.dtype.type(0.75) if a.dtype.kind == "f" else a.copy()) for n, a in ins.items()}
+    want2 = {n: a.copy() for n, a in ins2.items()}
+    oracle_cpu.run(spec, want2, w.scalars, "accsat", fma=True, f32=dtype == "f32")
+    for n in ins2:
+        host[n].copy_(torch.from_numpy(ins2[n]))
+    r.run(dict(w.scalars), "accsat")
+    torch.cuda.synchronize()
+    for n in ins2:
+        assert bitwise_equal(host[n].numpy(), want2[n]), f"{kid} chunks={chunks} (second call): '{n}'"
