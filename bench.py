@@ -48,6 +48,7 @@ TABLE = [
     ("clover.c:pdv_predict:1", 7680, "f64", 1),
     ("clover.c:advec_cell_x:2", 7680, "f64", 1),
     ("wave4.c:wave4:0", 1024, "f32", 1),
+    ("zsolve.c:z_solve_lhs:0", 256, "f64", 1),
 ]
 
 REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",

@@ -34,7 +34,7 @@ ROOT = os.path.dirname(HERE)
 sys.path.insert(0, ROOT)
 from paper_2306_13002_b200 import kernel_subset as ks  # noqa: E402
 
-NESTS = ["jacobi7", "swim", "clover", "wave4", "d3q19"]
+NESTS = ["jacobi7", "swim", "clover", "wave4", "d3q19", "zsolve"]
 F32_NESTS = {"wave4"}
 # (form name, source variant or None for the original text, fma rewrite)
 FORMS = [("original", None, False), ("cse", "cse", False), ("cse_bulk", "cse+bulk", False),

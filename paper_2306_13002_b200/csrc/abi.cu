@@ -19,6 +19,7 @@ void register_swim();
 void register_clover();
 void register_wave4();
 void register_d3q19();
+void register_zsolve();
 
 namespace {
 thread_local std::string g_err;
@@ -34,6 +35,7 @@ void init_registry() {
         register_clover();
         register_wave4();
         register_d3q19();
+        register_zsolve();
     });
 }
 }  // namespace

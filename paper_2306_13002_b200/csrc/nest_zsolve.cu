@@ -1,0 +1,26 @@
+// Registration of the zsolve nest function (generated body: gen/zsolve.cuh).
+// NPB-BT z_solve LHS: 50 loaded component fields (fjacZ/njacZ at k-1, k, k+1)
+// and 75 stored ones per point; every (m, n[, side]) component is its own
+// contiguous 3-D field, so the naive skeleton's loads are already coalesced
+// along j and the k-neighbour re-reads are L2 hits (three planes of the 50
+// loaded fields = 80 MB at 258^2 < 126 MB L2); the march skeleton stages the
+// 25-component boxes of both jacobians per k-plane through TMA instead.
+#include "registry.hpp"
+#include "kernels/march.cuh"
+#include "gen/zsolve.cuh"
+
+namespace acs {
+
+void register_zsolve() {
+    static Entry e;
+    e.kernel_id = "zsolve.c:z_solve_lhs:0";
+    e.function = "z_solve_lhs";
+    describe<gen::z_solve_lhs>(e, "zsolve.c", 0);
+    fill_naive<gen::z_solve_lhs, double>(e, 0);
+    fill_naive_occ<gen::z_solve_lhs, double, 4>(e, 0);
+    fill_march<gen::z_solve_lhs, double, 0, 32, 2, 32, 2, 1>(e, 0);
+    fill_march<gen::z_solve_lhs, double, 0, 64, 1, 64, 1, 1>(e, 0);
+    register_entry(&e);
+}
+
+}  // namespace acs

@@ -833,6 +833,7 @@ NEST_FUNCS = {
     "clover": ["ideal_gas", "pdv_predict", "advec_cell_x"],
     "wave4": ["wave4"],
     "d3q19": ["stream_collide"],
+    "zsolve": ["z_solve_lhs"],
 }
 
 

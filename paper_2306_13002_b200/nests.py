@@ -70,7 +70,7 @@ class KernelSpec:
 
 def _load_specs() -> Dict[str, KernelSpec]:
     out = {}
-    for nest in ("jacobi7", "swim", "clover", "wave4", "d3q19"):
+    for nest in ("jacobi7", "swim", "clover", "wave4", "d3q19", "zsolve"):
         with open(os.path.join(NEST_DIR, f"{nest}.c")) as f:
             mod = ks.parse(f.read())
         for reg in ks.find_regions(mod):
@@ -241,6 +241,20 @@ def workload(kernel_id: str, size=None, dtype: str = "f64") -> Workload:
                                ["mass_flux_x", "ener_flux"])}[f]
         bpp = 8 * (len(rw[0]) + len(rw[1]))
         return Workload(s, dims, sc, fills, "f64", ny * nx, bpp, rw[0], rw[1])
+    if s.nest == "zsolve":
+        # NPB-BT z_solve LHS.  Scalars as BT class-style constants (dt = 0.0008,
+        # tz1 = 1/dz^2, tz2 = 1/(2 dz) for dz = 1/(n+1); dz1..dz5 the BT
+        # dissipation coefficients); jacobians ~ U[-1, 1].
+        nz, ny, nx = _grid3(size or 256)
+        g = (nz + 2, ny + 2, nx + 2)
+        dims = {"fjacZ": (5, 5) + g, "njacZ": (5, 5) + g, "lhsZ": (5, 5, 3) + g}
+        h = 1.0 / (nz + 1)
+        sc = {"dt": 0.0008, "tz1": 1.0 / (h * h), "tz2": 1.0 / (2.0 * h), "dz1": 1.0, "dz2": 1.0, "dz3": 1.0,
+              "dz4": 1.0, "dz5": 1.0, "kbeg": 1, "kend": nz + 1, "ny": g[1], "nx": g[2]}
+        fills = {"fjacZ": Fill("uniform", -1.0, 1.0), "njacZ": Fill("uniform", -1.0, 1.0),
+                 "lhsZ": Fill("const", value=0.0)}
+        # 25 + 25 reads (each element once) + 75 writes of 8 B per point
+        return Workload(s, dims, sc, fills, "f64", nz * ny * nx, 8 * 125, ["fjacZ", "njacZ"], ["lhsZ"])
     raise KeyError(kernel_id)
 
 

@@ -35,6 +35,7 @@ SIZES = {
     "d3q19": [5, (3, 4, 6), (13, 17, 35)],
     "swim": [12, (9, 14), (131, 257)],
     "clover": [12, (7, 13), (131, 257)],
+    "zsolve": [4, (3, 2, 5), (9, 13, 37)],
 }
 
 

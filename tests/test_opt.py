@@ -25,7 +25,7 @@ from paper_2306_13002_b200 import nests, satopt
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF_TOOL = os.path.join(ROOT, "oracle", "_ref", "ref_tool")
-NESTS = ["jacobi7", "swim", "clover", "wave4", "d3q19"]
+NESTS = ["jacobi7", "swim", "clover", "wave4", "d3q19", "zsolve"]
 VARIANTS = ["cse", "cse+sat", "cse+bulk", "accsat"]
 
 

@@ -19,7 +19,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-NESTS = ["jacobi7", "swim", "clover", "wave4", "d3q19"]
+NESTS = ["jacobi7", "swim", "clover", "wave4", "d3q19", "zsolve"]
 VARIANTS = ["cse", "cse+sat", "cse+bulk", "accsat"]
 
 

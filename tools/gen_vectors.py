@@ -38,6 +38,7 @@ SIZES = {
     "d3q19": {"toy": 5, "ragged": (3, 4, 6)},
     "swim": {"toy": 12, "ragged": (9, 14)},
     "clover": {"toy": 12, "ragged": (7, 13)},
+    "zsolve": {"toy": 4, "ragged": (3, 2, 5)},
 }
 
 
