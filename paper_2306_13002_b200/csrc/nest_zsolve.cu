@@ -4,9 +4,12 @@
 // contiguous 3-D field, so the naive skeleton's loads are already coalesced
 // along j and the k-neighbour re-reads are L2 hits (three planes of the 50
 // loaded fields = 80 MB at 258^2 < 126 MB L2); the march skeleton stages the
-// 25-component boxes of both jacobians per k-plane through TMA instead.
+// 25-component boxes of both jacobians per k-plane through TMA; the sliced
+// skeleton gives each of the 25 independent (m, n) components its own
+// threads, marching k with the re-reads served by L1.
 #include "registry.hpp"
 #include "kernels/march.cuh"
+#include "kernels/sliced.cuh"
 #include "gen/zsolve.cuh"
 
 namespace acs {
@@ -17,8 +20,9 @@ void register_zsolve() {
     e.function = "z_solve_lhs";
     describe<gen::z_solve_lhs>(e, "zsolve.c", 0);
     fill_naive<gen::z_solve_lhs, double>(e, 0);
-    fill_naive_occ<gen::z_solve_lhs, double, 4>(e, 0);
-    fill_march<gen::z_solve_lhs, double, 0, 32, 2, 32, 2, 1>(e, 0);
+    fill_sliced<gen::z_solve_lhs, double, 128, 2, 32>(e, 0);
+    fill_sliced<gen::z_solve_lhs, double, 64, 4, 16>(e, 0);
+    fill_sliced<gen::z_solve_lhs, double, 128, 1, 64>(e, 0);
     fill_march<gen::z_solve_lhs, double, 0, 64, 1, 64, 1, 1>(e, 0);
     register_entry(&e);
 }

@@ -72,6 +72,9 @@ class Lowered:
     # unconditional static stores: (array, per-position offset) written at
     # EVERY point of the iteration space on every path (both arms of an if)
     must_write: set = field(default_factory=set)
+    # component slices: independent groups of stores (and the statements
+    # they need), each emitted as its own device body; [] = not sliceable
+    slices: List[str] = field(default_factory=list)
 
 
 class LowerError(Exception):
@@ -582,6 +585,118 @@ class _Lowerer:
             return {(key[0], offs)}
         return set()
 
+    # -- component slicing
+    #
+    # zsolve's 75 stores fall into 25 groups (one per 5x5 block entry m, n)
+    # that share no loaded element: lhsZ[m][n][*] reads only fjacZ[m][n] and
+    # njacZ[m][n].  Each group, with the statements its stores need (scalar
+    # temps duplicated), is an independent per-point body, so the skeleton can
+    # spread components over threads: 25x the parallelism, 1/25 of the live
+    # state per thread.  Exact: every stored value is computed by the same
+    # statements in the same order.
+
+    def _flat(self, s: ks.Stmt, out: List[ks.Stmt]) -> bool:
+        if s.kind == "block":
+            return all(self._flat(c, out) for c in s.stmts)
+        if s.kind in ("decl", "assign", "empty"):
+            out.append(s)
+            return True
+        return False
+
+    def _fields(self, e: Optional[ks.Expr], out: set):
+        if e is None:
+            return
+        if e.kind == "ref":
+            key = []
+            for p, idx in enumerate(e.kids):
+                a = self.as_affine(idx)
+                if a is None:
+                    key = None
+                    break
+                if a.var is None:
+                    key.append((p, a.off))
+            out.add((e.op, tuple(key) if key is not None else None))
+        for k in e.kids:
+            self._fields(k, out)
+
+    def slice_groups(self) -> Optional[List[List[ks.Stmt]]]:
+        stmts: List[ks.Stmt] = []
+        if not self._flat(self.body_stmt, stmts):
+            return None
+        names = [n for s_ in stmts if s_.kind == "decl" for n, _, _ in s_.names]
+        if len(names) != len(set(names)):
+            return None
+        assigns = [s_ for s_ in stmts if s_.kind == "assign"]
+        defs: Dict[str, ks.Stmt] = {}
+        for s_ in assigns:
+            if s_.lhs.kind == "var":
+                if s_.lhs.op in defs:
+                    return None                    # multiply-assigned scalar: keep whole
+                defs[s_.lhs.op] = s_
+        stores = [s_ for s_ in assigns if s_.lhs.kind == "ref"]
+        if len(stores) < 2 or (self.stored & self.loaded):
+            return None
+        order = {id(s_): i for i, s_ in enumerate(stmts)}
+        memo: Dict[int, set] = {}
+
+        def back(st: ks.Stmt) -> set:
+            if id(st) in memo:
+                return memo[id(st)]
+            out = {id(st)}
+            used = ks_vars(st.rhs) | (ks_vars(st.lhs) if st.lhs.kind == "ref" else set())
+            for v in used:
+                if v in defs:
+                    out |= back(defs[v])
+            memo[id(st)] = out
+            return out
+
+        by_id = {id(s_): s_ for s_ in stmts}
+        parent = list(range(len(stores)))
+
+        def find(a):
+            while parent[a] != a:
+                parent[a] = parent[parent[a]]
+                a = parent[a]
+            return a
+        owner: Dict[tuple, int] = {}
+        for i, st in enumerate(stores):
+            f: set = set()
+            for sid in back(st):
+                self._fields(by_id[sid].rhs, f)
+                if by_id[sid].lhs.kind == "ref":
+                    for idx in by_id[sid].lhs.kids:
+                        self._fields(idx, f)
+            for key in f:
+                if key in owner:
+                    parent[find(i)] = find(owner[key])
+                else:
+                    owner[key] = i
+        groups: Dict[int, set] = {}
+        for i, st in enumerate(stores):
+            groups.setdefault(find(i), set()).update(back(st))
+        if len(groups) < 2:
+            return None
+        decls = [s_ for s_ in stmts if s_.kind == "decl"]
+        out = []
+        for root in sorted(groups, key=lambda r: min(order[x] for x in groups[r])):
+            ids = sorted(groups[root], key=lambda x: order[x])
+            out.append(decls + [by_id[x] for x in ids])
+        return out
+
+    def emit_slices(self) -> List[str]:
+        groups = self.slice_groups()
+        if not groups:
+            return []
+        saved = (self.n_fma, self.n_loads, self.n_dyn)
+        bodies = []
+        for g in groups:
+            out: List[str] = ["    " + x for x in self.pre]   # function-level locals (temp1, ...)
+            for st in g:
+                self.st(st, 2, out)
+            bodies.append("\n".join(out))
+        self.n_fma, self.n_loads, self.n_dyn = saved
+        return bodies
+
     def bound_expr(self, e: ks.Expr) -> str:
         c, t = self.ex(e)
         if t != "int":
@@ -631,14 +746,16 @@ class _Lowerer:
             elif s.kind != "empty":
                 raise LowerError("statements outside the loop nest are not supported")
         bounds = self.loop_bounds()
+        self.pre = pre
         out: List[str] = list(pre)
         self.st(body_stmt, 1, out)
         must = self.must_write(body_stmt)
+        slices = self.emit_slices()
         sig = {a: self.sig.get(a) for a in self.arrays}
         return Lowered(self.fn.name, self.fn.params, self.loop_vars, bounds,
                        {a: (s if s is not None else [-1] * len(self.arrays[a].dims)) for a, s in sig.items()},
                        self.stored, "\n".join(out), self.n_fma, self.n_loads, self.n_dyn, self.offrange,
-                       self.ldrange, self.dynrange, self.dynsig, self.loaded, must)
+                       self.ldrange, self.dynrange, self.dynsig, self.loaded, must, slices)
 
 
 def lower_text(text: str, function: str, fma: bool, f32: bool = False, ifconv: bool = True) -> Lowered:
@@ -737,7 +854,22 @@ def gen_function(nest: str, function: str, f32: bool = False) -> Tuple[str, dict
             L.append(f"    {ty} {p.name} = s_.{p.name}; (void){p.name};")
         L.append(low.body)
         L.append("}")
-        meta[form] = {"loads": low.n_loads, "dyn_loads": low.n_dyn_loads, "fma": low.n_fma}
+        meta[form] = {"loads": low.n_loads, "dyn_loads": low.n_dyn_loads, "fma": low.n_fma,
+                      "slices": max(1, len(low.slices))}
+        L.append(f"// form {form}: {max(1, len(low.slices))} independent component slice(s)")
+        L.append(f"template <int SLICE, class M>")
+        L.append(f"static __device__ __forceinline__ void body_{form}_slice(M& m, const Scalars& s_, {lv}) {{")
+        if low.slices:
+            for p in sc:
+                ty = "int" if p.ty == "int" else ("float" if f32 else "double")
+                L.append(f"    {ty} {p.name} = s_.{p.name}; (void){p.name};")
+            for si, b in enumerate(low.slices):
+                L.append(f"    {'if' if si == 0 else 'else if'} constexpr (SLICE == {si}) {{")
+                L.append(b)
+                L.append("    }")
+        else:
+            L.append(f"    body_{form}(m, s_, {', '.join(low.loop_vars)});")
+        L.append("}")
     forms = [f for f, _, _ in FORMS]
     L.append("// per acs_variant (ORIGINAL, CSE, CSE_BULK, CSE_SAT, ACCSAT)")
     L.append("static constexpr int static_loads[5] = {" + ", ".join(str(meta[f]["loads"]) for f in forms) + "};")
@@ -817,6 +949,14 @@ def gen_function(nest: str, function: str, f32: bool = False) -> Tuple[str, dict
              + (", ".join(row(list(o)) for _, o in must) if must else row([])) + "};")
     L.append("static constexpr bool has_dynamic_index = " + ("true" if any(m_["dyn_loads"] for m_ in meta.values()) else "false") + ";")
     args = ", ".join(f"pt[{d}]" for d in range(len(base.loop_vars)))
+    L.append("// component slices per acs_variant (1 = the whole body)")
+    L.append("static constexpr int nslices[5] = {" + ", ".join(str(meta[f]["slices"]) for f in forms) + "};")
+    L.append("template <int FORM, int SLICE, class M>")
+    L.append("static __device__ __forceinline__ void body_slice(M& m, const Scalars& s, const int* pt) {")
+    for fi, f in enumerate(forms):
+        kw = "if" if fi == 0 else "else if"
+        L.append(f"    {kw} constexpr (FORM == {fi}) body_{f}_slice<SLICE>(m, s, {args});")
+    L.append("}")
     L.append("template <int FORM, class M>")
     L.append("static __device__ __forceinline__ void body(M& m, const Scalars& s, const int* pt) {")
     for fi, f in enumerate(forms):
