@@ -32,11 +32,29 @@ namespace acs {
 
 // LAYOUT 0: row-major (reference layout, optionally with padded pitches);
 // LAYOUT 1: trailing subscript slowest (D3Q19 q-major SoA).
-template <class NS, class T, int LAYOUT, int TX, int TY>
+template <class NS, class T, int LAYOUT, int TX, int TY, int RX = 1>
 struct MarchPlan {
     static constexpr int NL = NS::NLOOP;
     static constexpr int X = NL - 1;   // loop index of the innermost loop (tile x)
     static constexpr int Y = NL == 3 ? 1 : -9;
+    // RX > 1 (register windows): the tile origin is aligned down to a 16-byte
+    // element multiple V and every staged array's box starts RA elements
+    // below it (RA = the largest x reach below the point, rounded up to V), so
+    // a thread's point group and every window row sit at compile-time-known
+    // alignment.
+    static constexpr bool ALIGNED = RX > 1;
+    static constexpr int V = 16 / (int)sizeof(T);
+    static constexpr int ra() {
+        int r = 0;
+        for (int a = 0; a < NS::NARR; ++a)
+            if (NS::stageable(a))
+                for (int p = 0; p < NS::ndim(a); ++p)
+                    if (NS::ld_sig(a, p) == X && -NS::ld_lo(a, p) > r) r = -NS::ld_lo(a, p);
+        return (r + V - 1) / V * V;
+    }
+    static constexpr int RA = ra();
+    // box origin of array a at position p, relative to the tile's point
+    static constexpr int lo(int a, int p) { return ALIGNED && NS::ld_sig(a, p) == X ? -RA : NS::ld_lo(a, p); }
 
     static constexpr int esize(int a) { return NS::is_int(a) ? 4 : (int)sizeof(T); }
     // LAYOUT 1 applies to arrays whose trailing subscript is a component index
@@ -67,7 +85,7 @@ struct MarchPlan {
     }
     static constexpr int raw_extent(int a, int p) {
         const int s = NS::ld_sig(a, p);
-        const int w = NS::ld_hi(a, p) - NS::ld_lo(a, p);
+        const int w = NS::ld_hi(a, p) - lo(a, p);
         if (s == 0) return 1;
         if (s == X) return TX + w;
         if (s == Y) return TY + w;
@@ -84,7 +102,7 @@ struct MarchPlan {
         const int e = raw_extent(a, p);
         if (p != pos_of_dim(a, 0)) return e;
         const int q = xq(a);
-        const int need = inner_is_x(a) ? e + q - 1 : e;
+        const int need = inner_is_x(a) && !ALIGNED ? e + q - 1 : e;
         return (need + q - 1) / q * q;
     }
     static constexpr int bstride(int a, int p) {   // element stride of position p inside the box
@@ -146,10 +164,11 @@ struct TmaMaps {
 };
 
 // per-CTA state a body's memory policy needs
-template <class NS, class T, int LAYOUT, int TX, int TY, int PF>
+template <class NS, class T, int LAYOUT, int TX, int TY, int PF, int RX = 1>
 struct MarchMem {
-    using P = MarchPlan<NS, T, LAYOUT, TX, TY>;
+    using P = MarchPlan<NS, T, LAYOUT, TX, TY, RX>;
     static constexpr int D = P::maxspan() + PF;
+    using value_t = T;
     NaiveMem<NS, T, false> g;
     const unsigned char* ring;     // slot 0
     const unsigned char* stat;     // static boxes
@@ -182,7 +201,7 @@ struct MarchMem {
 #pragma unroll
             for (int p = 0; p < (int)sizeof...(O); ++p) {
                 const int s = NS::ld_sig(ARR, p);
-                const int l = off[p] - NS::ld_lo(ARR, p);
+                const int l = off[p] - P::lo(ARR, p);
                 if (s == 0) delta = D + off[p] - NS::ld_hi(ARR, p);
                 else if (s == P::X) idx += (lx + l + sh[ARR]) * P::bstride(ARR, p);
                 else if (s == P::Y) idx += (ly + l) * P::bstride(ARR, p);
@@ -193,6 +212,27 @@ struct MarchMem {
         } else {
             return g.template ld<ARR, O...>();
         }
+    }
+
+    // start of row R's window in its staged box for the point at tile x lx
+    // (the RX-window path: alignment shift 0)
+    template <int R>
+    __device__ __forceinline__ const T* row_ptr(int lx) const {
+        constexpr int A = NS::row_arr(R);
+        int idx = 0;
+        int delta = D;
+#pragma unroll
+        for (int p = 0; p < NS::ndim(A); ++p) {
+            const int s = NS::ld_sig(A, p);
+            const int o = s == P::X ? NS::row_xlo(R) : NS::row_off(R, p);
+            const int l = o - P::lo(A, p);
+            if (s == 0) delta = D + o - NS::ld_hi(A, p);
+            else if (s == P::X) idx += (lx + l) * P::bstride(A, p);
+            else if (s == P::Y) idx += (ly + l) * P::bstride(A, p);
+            else idx += l * P::bstride(A, p);
+        }
+        if (delta >= D) delta -= D;
+        return reinterpret_cast<const T*>(box_base<A>(delta)) + idx;
     }
 
     // out-of-box dynamic index: rare (e.g. advec's clamp at the domain edge),
@@ -209,7 +249,7 @@ struct MarchMem {
 #pragma unroll
             for (int p = 0; p < (int)sizeof...(I); ++p) {
                 const int s = NS::ld_sig(ARR, p);
-                const int lo = NS::ld_lo(ARR, p);
+                const int lo = P::lo(ARR, p);
                 if (s == 0) {
                     const int d = v[p] - k;
                     out |= (unsigned)(d - lo) > (unsigned)(NS::ld_hi(ARR, p) - lo);
@@ -235,9 +275,151 @@ struct MarchMem {
     __device__ __forceinline__ void stx(A... args) const { g.template stx<ARR>(args...); }
 };
 
+// ---- register windows (RX adjacent x points per thread) -------------------
+//
+// Per march step a thread loads, for every static-load ROW of the body (the
+// lowering's row table: array + subscript offsets other than the innermost
+// x), the RX + (xhi - xlo) consecutive elements its RX points read, with
+// 16-byte vector LDS (LDS.128), into registers; the per-point body then reads
+// them by compile-time index.  wave4 (13-point star, f32, RX = 4): 11 rows x
+// 2-3 LDS.128 per 4 points instead of 15 scalar LDS + address math per
+// point.  Needs every box row 16-byte aligned at the tile origin (the
+// per-array alignment shift sh == 0, true when the x loop starts at -ld_lo,
+// i.e. ghost width = stencil radius); otherwise the kernel takes the
+// per-point path.
+template <class NS, class T, int LAYOUT, int TX, int TY, int FORM, int RX>
+struct WinPlan {
+    using P = MarchPlan<NS, T, LAYOUT, TX, TY, RX>;
+    static constexpr int V = 16 / (int)sizeof(T);
+    static constexpr int xpos(int a) {
+        for (int p = 0; p < NS::ndim(a); ++p)
+            if (NS::ld_sig(a, p) == P::X) return p;
+        return -1;
+    }
+    static constexpr bool row_on(int r) {
+        return ((NS::row_forms(r) >> FORM) & 1) && P::staged(NS::row_arr(r)) && xpos(NS::row_arr(r)) >= 0;
+    }
+    static constexpr int width(int r) { return RX + NS::row_xhi(r) - NS::row_xlo(r); }
+    static constexpr int woff(int r) {
+        int o = 0;
+        for (int b = 0; b < r; ++b)
+            if (row_on(b)) o += width(b);
+        return o;
+    }
+    static constexpr int total() { return woff(NS::NROW); }
+    static constexpr int RXV = RX / V;
+    static constexpr int align(int r) {   // misalignment (elements) of the window start in its box row
+        const int a = NS::row_arr(r);
+        const int m = NS::row_xlo(r) - P::lo(a, xpos(a));
+        return ((m % V) + V) % V;
+    }
+    template <int ARR, int... O>
+    static constexpr int row_of() {
+        constexpr int off[sizeof...(O)] = {O...};
+        for (int r = 0; r < NS::NROW; ++r) {
+            if (NS::row_arr(r) != ARR || !row_on(r)) continue;
+            bool ok = true;
+            for (int p = 0; p < (int)sizeof...(O); ++p)
+                if (p != xpos(ARR) && NS::row_off(r, p) != off[p]) ok = false;
+            if (ok) return r;
+        }
+        return -1;
+    }
+    // deferred vector stores: static store targets of arrays the nest never
+    // loads, at an x offset that keeps the point group 16-byte aligned
+    static constexpr int sxpos(int a) {
+        for (int p = 0; p < NS::ndim(a); ++p)
+            if (NS::sig(a, p) == P::X) return p;
+        return -1;
+    }
+    static constexpr bool srow_on(int r) {
+        const int a = NS::srow_arr(r);
+        return ((NS::srow_forms(r) >> FORM) & 1) && !NS::is_loaded(a) && !NS::is_int(a) && sxpos(a) >= 0 &&
+               NS::srow_off(r, sxpos(a)) % V == 0;
+    }
+    static constexpr int soff(int r) {
+        int o = 0;
+        for (int b = 0; b < r; ++b)
+            if (srow_on(b)) o += RX;
+        return o;
+    }
+    static constexpr int stotal() { return soff(NS::NSROW); }
+    template <int ARR, int... O>
+    static constexpr int srow_of() {
+        constexpr int off[sizeof...(O)] = {O...};
+        for (int r = 0; r < NS::NSROW; ++r) {
+            if (NS::srow_arr(r) != ARR || !srow_on(r)) continue;
+            bool ok = true;
+            for (int p = 0; p < (int)sizeof...(O); ++p)
+                if (NS::srow_off(r, p) != off[p]) ok = false;
+            if (ok) return r;
+        }
+        return -1;
+    }
+    template <int R, class G, int... PP>
+    static __device__ __forceinline__ long long sidx(const G& g, std::integer_sequence<int, PP...>) {
+        return g.template static_index<NS::srow_arr(R), NS::srow_off(R, PP)...>();
+    }
+    static constexpr bool usable() {
+        if (RX <= 1) return false;
+        if (LAYOUT != 0 || RX % V != 0 || TX % RX != 0) return false;
+        for (int r = 0; r < NS::NROW; ++r)
+            if (row_on(r) && NS::is_int(NS::row_arr(r))) return false;
+        return total() > 0 && total() <= 160;
+    }
+};
+
+// per-point view of the windows: point R0 of the thread's RX group
+template <class MM, class WP, class NS, int R0>
+struct WinMem {
+    const MM& m;
+    const typename MM::value_t* win;
+    typename MM::value_t* out;     // deferred stores of the point group
+    bool defer;
+    template <int ARR>
+    using elem_t = typename MM::template elem_t<ARR>;
+    template <int ARR, int... O>
+    __device__ __forceinline__ elem_t<ARR> ld() const {
+        constexpr int r = WP::template row_of<ARR, O...>();
+        if constexpr (r >= 0) {
+            constexpr int off[sizeof...(O)] = {O...};
+            constexpr int ox = off[WP::xpos(ARR)];
+            return win[WP::woff(r) + R0 + ox - NS::row_xlo(r)];
+        } else {
+            return m.template ld<ARR, O...>();
+        }
+    }
+    template <int ARR, class... I>
+    __device__ __forceinline__ elem_t<ARR> ldx(I... ii) const { return m.template ldx<ARR>(ii...); }
+    template <int ARR, int... O>
+    __device__ __forceinline__ void st(elem_t<ARR> v) const {
+        constexpr int r = WP::template srow_of<ARR, O...>();
+        if constexpr (r >= 0) {
+            if (defer) {
+                out[WP::soff(r) + R0] = v;
+                return;
+            }
+        }
+        m.template st<ARR, O...>(v);
+    }
+    template <int ARR, class... A>
+    __device__ __forceinline__ void stx(A... args) const { m.template stx<ARR>(args...); }
+};
+
+template <class T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+    using type = float4;
+};
+template <>
+struct Vec16<double> {
+    using type = double2;
+};
+
 template <class P, class NS>
 __host__ __device__ constexpr int xshift(int a, int orgx) {
-    if (!P::inner_is_x(a)) return 0;
+    if (P::ALIGNED || !P::inner_is_x(a)) return 0;
     const int q = P::xq(a);
     const int v = orgx + NS::ld_lo(a, P::pos_of_dim(a, 0));
     return ((v % q) + q) % q;
@@ -257,7 +439,7 @@ __device__ __forceinline__ void march_issue(unsigned char* slot_base, const TmaM
                     const int p = P::pos_of_dim(A, d);
                     const int s = NS::ld_sig(A, p);
                     if (s == 0) c[d] = plane_base + NS::ld_hi(A, p);
-                    else if (s == P::X) c[d] = orgx + NS::ld_lo(A, p) - (d == 0 ? xshift<P, NS>(A, orgx) : 0);
+                    else if (s == P::X) c[d] = orgx + P::lo(A, p) - (d == 0 ? xshift<P, NS>(A, orgx) : 0);
                     else if (s == P::Y) c[d] = orgy + NS::ld_lo(A, p);
                     else c[d] = NS::ld_lo(A, p);
                 }
@@ -271,12 +453,65 @@ __device__ __forceinline__ void march_issue(unsigned char* slot_base, const TmaM
 
 // TX x TY points per tile, BX x BY threads: each thread computes (TX/BX) x (TY/BY)
 // points per march step, amortising the step's barrier / mbarrier wait.
-template <class NS, class T, int FORM, int LAYOUT, int TX, int TY, int BX, int BY, int PF>
+template <class WP, class MM, class NS, int FORM, int R0, int RX>
+__device__ __forceinline__ void win_run(MM& m, const typename MM::value_t* win, typename MM::value_t* out,
+                                        bool defer, const KernelArgs<NS>& args, int* pt, int lx0, int xlo, int xhi) {
+    if constexpr (R0 < RX) {
+        const int x = m.orgx + lx0 + R0;
+        if (x < xhi && x >= xlo) {
+            pt[NS::NLOOP - 1] = x;
+            m.lx = lx0 + R0;
+            WinMem<MM, WP, NS, R0> wm{m, win, out, defer};
+            NS::template body<FORM>(wm, args.s, pt);
+        }
+        win_run<WP, MM, NS, FORM, R0 + 1, RX>(m, win, out, defer, args, pt, lx0, xlo, xhi);
+    }
+}
+
+// the group's deferred stores: one 16-byte vector store per V points
+template <class WP, class MM, class NS, int R>
+__device__ __forceinline__ void win_flush(const MM& m, const typename MM::value_t* out) {
+    if constexpr (R < NS::NSROW) {
+        if constexpr (WP::srow_on(R)) {
+            using E = typename MM::value_t;
+            using VT = typename Vec16<E>::type;
+            constexpr int A = NS::srow_arr(R);
+            const long long idx = WP::template sidx<R>(m.g, std::make_integer_sequence<int, NS::ndim(A)>{});
+            E* p = reinterpret_cast<E*>(m.g.a.arr[A].base) + idx;
+#pragma unroll
+            for (int v = 0; v < WP::RXV; ++v)
+                *reinterpret_cast<VT*>(p + v * WP::V) = *reinterpret_cast<const VT*>(&out[WP::soff(R) + v * WP::V]);
+        }
+        win_flush<WP, MM, NS, R + 1>(m, out);
+    }
+}
+
+template <class WP, class MM, class NS, int R>
+__device__ __forceinline__ void win_load(const MM& m, typename MM::value_t* win, int lx0) {
+    if constexpr (R < NS::NROW) {
+        if constexpr (WP::row_on(R)) {
+            using E = typename MM::value_t;
+            using VT = typename Vec16<E>::type;
+            constexpr int V = WP::V, A = WP::align(R), W = WP::width(R);
+            constexpr int NV = (A + W + V - 1) / V;
+            const E* p = m.template row_ptr<R>(lx0) - A;
+            E tmp[NV * V];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) *reinterpret_cast<VT*>(&tmp[v * V]) = *reinterpret_cast<const VT*>(p + v * V);
+#pragma unroll
+            for (int w = 0; w < W; ++w) win[WP::woff(R) + w] = tmp[A + w];
+        }
+        win_load<WP, MM, NS, R + 1>(m, win, lx0);
+    }
+}
+
+template <class NS, class T, int FORM, int LAYOUT, int TX, int TY, int BX, int BY, int PF, int RX = 1>
 __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ KernelArgs<NS> args,
                                                        const __grid_constant__ TmaMaps<NS> maps, int kchunk) {
     static_assert(TX % BX == 0 && TY % BY == 0, "tile must be a multiple of the block");
-    using P = MarchPlan<NS, T, LAYOUT, TX, TY>;
-    using M = MarchMem<NS, T, LAYOUT, TX, TY, PF>;
+    static_assert(RX == 1 || TX == BX * RX, "register windows: one RX group of adjacent points per thread");
+    using P = MarchPlan<NS, T, LAYOUT, TX, TY, RX>;
+    using M = MarchMem<NS, T, LAYOUT, TX, TY, PF, RX>;
     constexpr int D = M::D;
     constexpr int MS = P::maxspan();
     extern __shared__ __align__(128) unsigned char smem[];
@@ -286,7 +521,8 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * BX + tx;
-    const int orgx = args.lo[P::X] + blockIdx.x * TX;
+    const int xlo0 = (int)args.lo[P::X];
+    const int orgx = (P::ALIGNED ? xlo0 - (((xlo0 % P::V) + P::V) % P::V) : xlo0) + blockIdx.x * TX;
     const int orgy = NS::NLOOP == 3 ? args.lo[1] + blockIdx.y * TY : 0;
     const int kb = args.lo[0] + blockIdx.z * kchunk;
     const int ke = min(kb + kchunk, args.hi[0]);
@@ -316,8 +552,27 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
 
     int pt[NS::NLOOP];
     M m{NaiveMem<NS, T, false>{args, pt}, ring, stat, 0, tx, ty, 0, orgx, orgy, {}};
+    bool aligned = true;
 #pragma unroll
-    for (int a = 0; a < NS::NARR; ++a) m.sh[a] = xshift<P, NS>(a, orgx);
+    for (int a = 0; a < NS::NARR; ++a) {
+        m.sh[a] = xshift<P, NS>(a, orgx);
+        if (P::staged(a) && m.sh[a] != 0) aligned = false;
+    }
+    using WP = WinPlan<NS, T, LAYOUT, TX, TY, FORM, RX>;
+    bool vec_ok = false;
+    if constexpr (WP::usable()) {
+        vec_ok = !args.sh.enabled;
+#pragma unroll
+        for (int r = 0; r < NS::NSROW; ++r) {
+            if (!WP::srow_on(r)) continue;
+            const int a = NS::srow_arr(r);
+            if (reinterpret_cast<uintptr_t>(args.arr[a].base) % 16 != 0) vec_ok = false;
+            for (int p = 0; p < NS::ndim(a); ++p) {
+                const long long st = args.arr[a].stride[p];
+                if (p == WP::sxpos(a) ? st != 1 : st % WP::V != 0) vec_ok = false;
+            }
+        }
+    }
 
     for (int s = 0; s < ns; ++s) {
         __syncthreads();   // every thread is done with step s-1: its oldest slot is free
@@ -335,14 +590,38 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
         pt[0] = kb + s;
         m.k = kb + s;
         m.newest = Bw % D;
+        if constexpr (WP::usable()) {
+            if (aligned) {
+#pragma unroll
+                for (int ry = 0; ry < TY / BY; ++ry) {
+                    m.ly = ty + ry * BY;
+                    const int y = orgy + m.ly;
+                    if (NS::NLOOP == 3 && y >= args.hi[1]) continue;
+                    if constexpr (NS::NLOOP == 3) pt[1] = y;
+                    T win[WP::total()];
+                    T out[WP::stotal() > 0 ? WP::stotal() : 1];
+                    win_load<WP, M, NS, 0>(m, win, tx * RX);
+                    const int x0 = orgx + tx * RX;
+                    const bool defer = vec_ok && x0 >= xlo0 && x0 + RX <= args.hi[P::X];
+                    win_run<WP, M, NS, FORM, 0, RX>(m, win, out, defer, args, pt, tx * RX, xlo0, args.hi[P::X]);
+                    if constexpr (WP::stotal() > 0) {
+                        if (defer) {
+                            pt[P::X] = x0;
+                            win_flush<WP, M, NS, 0>(m, out);
+                        }
+                    }
+                }
+                continue;
+            }
+        }
 #pragma unroll
         for (int ry = 0; ry < TY / BY; ++ry) {
 #pragma unroll
             for (int rx = 0; rx < TX / BX; ++rx) {
-                m.lx = tx + rx * BX;
+                m.lx = RX > 1 ? tx * RX + rx : tx + rx * BX;
                 m.ly = ty + ry * BY;
                 const int x = orgx + m.lx, y = orgy + m.ly;
-                if (x < args.hi[P::X] && (NS::NLOOP < 3 || y < args.hi[1])) {
+                if (x < args.hi[P::X] && x >= xlo0 && (NS::NLOOP < 3 || y < args.hi[1])) {
                     pt[P::X] = x;
                     if constexpr (NS::NLOOP == 3) pt[1] = y;
                     NS::template body<FORM>(m, args.s, pt);
@@ -364,9 +643,9 @@ inline bool acs_debug() {
         return false;                                                                       \
     } while (0)
 
-template <class NS, class T, int LAYOUT, int TX, int TY>
+template <class NS, class T, int LAYOUT, int TX, int TY, int RX = 1>
 bool encode_maps(const LaunchReq& r, TmaMaps<NS>& maps) {
-    using P = MarchPlan<NS, T, LAYOUT, TX, TY>;
+    using P = MarchPlan<NS, T, LAYOUT, TX, TY, RX>;
     EncodeTiledFn enc = tma_encoder();
     if (!enc) {
         if (acs_debug()) std::fprintf(stderr, "[acs] no cuTensorMapEncodeTiled entry point\n");
@@ -427,9 +706,9 @@ bool encode_maps(const LaunchReq& r, TmaMaps<NS>& maps) {
     return true;
 }
 
-template <class NS, class T, int FORM, int LAYOUT, int TX, int TY, int BX, int BY, int PF>
+template <class NS, class T, int FORM, int LAYOUT, int TX, int TY, int BX, int BY, int PF, int RX = 1>
 acs_status launch_march(const LaunchReq& r) {
-    using P = MarchPlan<NS, T, LAYOUT, TX, TY>;
+    using P = MarchPlan<NS, T, LAYOUT, TX, TY, RX>;
     static_assert(P::usable(), "march skeleton: nest not stageable");
     KernelArgs<NS> ka;
     bool empty = false;
@@ -437,21 +716,22 @@ acs_status launch_march(const LaunchReq& r) {
     if (st != ACS_OK || empty) return st;
     TmaMaps<NS> maps;
     std::memset(&maps, 0, sizeof maps);
-    if (!encode_maps<NS, T, LAYOUT, TX, TY>(r, maps)) {
+    if (!encode_maps<NS, T, LAYOUT, TX, TY, RX>(r, maps)) {
         // layout the TMA cannot describe (unaligned base / pitch): same
         // numerics through the global-memory skeleton
         return launch_naive<NS, T, FORM>(r);
     }
     constexpr int D = P::maxspan() + PF;
     constexpr int smem = D * P::slot_bytes() + P::static_bytes() + (D + 1) * 8;
-    auto kern = march_kernel<NS, T, FORM, LAYOUT, TX, TY, BX, BY, PF>;
+    auto kern = march_kernel<NS, T, FORM, LAYOUT, TX, TY, BX, BY, PF, RX>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
     constexpr int NL = NS::NLOOP;
-    const long long nx = ka.hi[NL - 1] - ka.lo[NL - 1];
+    const long long xlo0 = ka.lo[NL - 1];
+    const long long nx = ka.hi[NL - 1] - (P::ALIGNED ? xlo0 - (((xlo0 % P::V) + P::V) % P::V) : xlo0);
     const long long ny = NL == 3 ? ka.hi[1] - ka.lo[1] : 1;
     const long long nz = ka.hi[0] - ka.lo[0];
     const long long tiles = ((nx + TX - 1) / TX) * (NL == 3 ? (ny + TY - 1) / TY : 1);
@@ -467,16 +747,17 @@ acs_status launch_march(const LaunchReq& r) {
     return check_launch("march");
 }
 
-template <class NS, class T, int LAYOUT, int TX, int TY, int BX, int BY, int PF>
+template <class NS, class T, int LAYOUT, int TX, int TY, int BX, int BY, int PF, int RX = 1>
 void fill_march(Entry& e, int prec) {
     const int slot = e.n_sched[prec]++;
-    e.launch[prec][0][slot] = &launch_march<NS, T, 0, LAYOUT, TX, TY, BX, BY, PF>;
-    e.launch[prec][1][slot] = &launch_march<NS, T, 1, LAYOUT, TX, TY, BX, BY, PF>;
-    e.launch[prec][2][slot] = &launch_march<NS, T, 2, LAYOUT, TX, TY, BX, BY, PF>;
-    e.launch[prec][3][slot] = &launch_march<NS, T, 3, LAYOUT, TX, TY, BX, BY, PF>;
-    e.launch[prec][4][slot] = &launch_march<NS, T, 4, LAYOUT, TX, TY, BX, BY, PF>;
+    e.launch[prec][0][slot] = &launch_march<NS, T, 0, LAYOUT, TX, TY, BX, BY, PF, RX>;
+    e.launch[prec][1][slot] = &launch_march<NS, T, 1, LAYOUT, TX, TY, BX, BY, PF, RX>;
+    e.launch[prec][2][slot] = &launch_march<NS, T, 2, LAYOUT, TX, TY, BX, BY, PF, RX>;
+    e.launch[prec][3][slot] = &launch_march<NS, T, 3, LAYOUT, TX, TY, BX, BY, PF, RX>;
+    e.launch[prec][4][slot] = &launch_march<NS, T, 4, LAYOUT, TX, TY, BX, BY, PF, RX>;
     e.sched_name[prec][slot] = "march tile " + std::to_string(TX) + "x" + std::to_string(TY) + " block " +
-                               std::to_string(BX) + "x" + std::to_string(BY) + " pf " + std::to_string(PF);
+                               std::to_string(BX) + "x" + std::to_string(BY) + " pf " + std::to_string(PF) +
+                               (RX > 1 ? " regwin " + std::to_string(RX) : "");
     for (int v = 0; v < 5; ++v)
         if (e.best[prec][v] == 0 && v != ACS_ORIGINAL) e.best[prec][v] = slot;
 }

@@ -23,7 +23,6 @@ void register_zsolve() {
     fill_sliced<gen::z_solve_lhs, double, 128, 2, 32>(e, 0);
     fill_sliced<gen::z_solve_lhs, double, 64, 4, 16>(e, 0);
     fill_sliced<gen::z_solve_lhs, double, 128, 1, 64>(e, 0);
-    fill_march<gen::z_solve_lhs, double, 0, 64, 1, 64, 1, 1>(e, 0);
     register_entry(&e);
 }
 

@@ -75,6 +75,8 @@ class Lowered:
     # component slices: independent groups of stores (and the statements
     # they need), each emitted as its own device body; [] = not sliceable
     slices: List[str] = field(default_factory=list)
+    static_refs: set = field(default_factory=set)    # distinct (array, offsets) of static loads
+    static_stores: set = field(default_factory=set)  # distinct (array, offsets) of static stores
 
 
 class LowerError(Exception):
@@ -134,6 +136,8 @@ class _Lowerer:
         self.n_ifc = 0
         self.ifconv = ifconv
         self.body_stmt: Optional[ks.Stmt] = None
+        self.static_refs: set = set()
+        self.static_stores: set = set()
 
     # -- types
     def real(self) -> str:
@@ -333,6 +337,7 @@ class _Lowerer:
             for p, o in enumerate(offs):
                 r[p][0] = min(r[p][0], o)
                 r[p][1] = max(r[p][1], o)
+            self.static_refs.add((e.op, tuple(offs)))
             return f"m.template ld<{arr}, {', '.join(str(o) for o in offs)}>()"
         self.record_dynamic(e)
         self.n_dyn += 1
@@ -401,6 +406,7 @@ class _Lowerer:
                     out.append(f"{pad}{self.capture[self.target_key(s.lhs)]} = {val};")
                     return
                 if offs is not None:
+                    self.static_stores.add((arr, tuple(offs)))
                     out.append(f"{pad}m.template st<ARR_{arr}, {', '.join(map(str, offs))}>({val});")
                 else:
                     idx = ", ".join(self.conv(*self.ex(i), "int") for i in s.lhs.kids)
@@ -755,7 +761,8 @@ class _Lowerer:
         return Lowered(self.fn.name, self.fn.params, self.loop_vars, bounds,
                        {a: (s if s is not None else [-1] * len(self.arrays[a].dims)) for a, s in sig.items()},
                        self.stored, "\n".join(out), self.n_fma, self.n_loads, self.n_dyn, self.offrange,
-                       self.ldrange, self.dynrange, self.dynsig, self.loaded, must, slices)
+                       self.ldrange, self.dynrange, self.dynsig, self.loaded, must, slices, self.static_refs,
+                       self.static_stores)
 
 
 def lower_text(text: str, function: str, fma: bool, f32: bool = False, ifconv: bool = True) -> Lowered:
@@ -947,6 +954,49 @@ def gen_function(nest: str, function: str, f32: bool = False) -> Tuple[str, dict
              + (", ".join(f"ARR_{a}" for a, _ in must) if must else "-1") + "};")
     L.append("static constexpr int must_write_off[" + str(max(1, len(must))) + "][8] = {"
              + (", ".join(row(list(o)) for _, o in must) if must else row([])) + "};")
+    # register-window rows (march skeleton, several adjacent x points per
+    # thread): distinct (array, subscript offsets except the innermost-loop
+    # position) of the static loads of every form, with the x-offset range
+    nl = len(base.loop_vars)
+    rowmap: Dict[tuple, List[int]] = {}
+    used: Dict[tuple, set] = {}
+    for fi, (form, low) in enumerate(lows.items()):
+        for arr, offs in low.static_refs:
+            sg = sig[arr]
+            xp = sg.index(nl - 1) if (nl - 1) in sg else -1
+            key = (names.index(arr), tuple(o if p != xp else 0 for p, o in enumerate(offs)))
+            ox = offs[xp] if xp >= 0 else 0
+            r = rowmap.setdefault(key, [ox, ox])
+            r[0], r[1] = min(r[0], ox), max(r[1], ox)
+            used.setdefault(key, set()).add(fi)
+    rkeys = sorted(rowmap)
+    L.append("// register-window rows: static-load rows (array, offsets with the innermost-loop position")
+    L.append("// zeroed), their x-offset range, and which forms (bit per acs_variant) read them")
+    L.append(f"static constexpr int NROW = {len(rkeys)};")
+    def tab(name, vals):
+        vals = list(vals) or [0]
+        L.append(f"static __host__ __device__ constexpr int {name}(int r) {{ constexpr int t[{len(vals)}] = {{"
+                 + ", ".join(str(v) for v in vals) + "}; return t[r]; }")
+    tab("row_arr", [k[0] for k in rkeys])
+    tab("row_xlo", [rowmap[k][0] for k in rkeys])
+    tab("row_xhi", [rowmap[k][1] for k in rkeys])
+    tab("row_forms", [sum(1 << f for f in used[k]) for k in rkeys])
+    offs_rows = [row(list(k[1])) for k in rkeys] or [row([])]
+    L.append(f"static __host__ __device__ constexpr int row_off(int r, int p) {{ constexpr int t[{len(offs_rows)}][8] = {{"
+             + ", ".join(offs_rows) + "}; return t[r][p]; }")
+    # store rows: distinct static store targets of every form (deferred
+    # vector stores of a thread's adjacent points)
+    srow: Dict[tuple, set] = {}
+    for fi, (form, low) in enumerate(lows.items()):
+        for arr, offs in low.static_stores:
+            srow.setdefault((names.index(arr), offs), set()).add(fi)
+    skeys = sorted(srow)
+    L.append(f"static constexpr int NSROW = {len(skeys)};")
+    tab("srow_arr", [k[0] for k in skeys])
+    tab("srow_forms", [sum(1 << f for f in srow[k]) for k in skeys])
+    soffs = [row(list(k[1])) for k in skeys] or [row([])]
+    L.append(f"static __host__ __device__ constexpr int srow_off(int r, int p) {{ constexpr int t[{len(soffs)}][8] = {{"
+             + ", ".join(soffs) + "}; return t[r][p]; }")
     L.append("static constexpr bool has_dynamic_index = " + ("true" if any(m_["dyn_loads"] for m_ in meta.values()) else "false") + ";")
     args = ", ".join(f"pt[{d}]" for d in range(len(base.loop_vars)))
     L.append("// component slices per acs_variant (1 = the whole body)")
