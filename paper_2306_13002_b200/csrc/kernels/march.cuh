@@ -214,21 +214,21 @@ struct MarchMem {
         }
     }
 
-    // start of row R's window in its staged box for the point at tile x lx
-    // (the RX-window path: alignment shift 0)
-    template <int R>
-    __device__ __forceinline__ const T* row_ptr(int lx) const {
-        constexpr int A = NS::row_arr(R);
+    // start of unique window K (WinPlan) in its staged box; lx0 / ly0 = the
+    // thread's first point (aligned-origin path: alignment shift 0)
+    template <class WP, int K>
+    __device__ __forceinline__ const T* uwin_ptr(int lx0, int ly0) const {
+        constexpr int A = WP::PL.u[K].arr;
         int idx = 0;
         int delta = D;
 #pragma unroll
         for (int p = 0; p < NS::ndim(A); ++p) {
             const int s = NS::ld_sig(A, p);
-            const int o = s == P::X ? NS::row_xlo(R) : NS::row_off(R, p);
+            const int o = s == P::X ? WP::PL.u[K].xlo : WP::u_off(K, p);
             const int l = o - P::lo(A, p);
             if (s == 0) delta = D + o - NS::ld_hi(A, p);
-            else if (s == P::X) idx += (lx + l) * P::bstride(A, p);
-            else if (s == P::Y) idx += (ly + l) * P::bstride(A, p);
+            else if (s == P::X) idx += (lx0 + l) * P::bstride(A, p);
+            else if (s == P::Y) idx += (ly0 + l) * P::bstride(A, p);
             else idx += l * P::bstride(A, p);
         }
         if (delta >= D) delta -= D;
@@ -275,42 +275,122 @@ struct MarchMem {
     __device__ __forceinline__ void stx(A... args) const { g.template stx<ARR>(args...); }
 };
 
-// ---- register windows (RX adjacent x points per thread) -------------------
+// ---- register windows: 2.5-D register blocking ------------------------------
 //
-// Per march step a thread loads, for every static-load ROW of the body (the
-// lowering's row table: array + subscript offsets other than the innermost
-// x), the RX + (xhi - xlo) consecutive elements its RX points read, with
-// 16-byte vector LDS (LDS.128), into registers; the per-point body then reads
-// them by compile-time index.  wave4 (13-point star, f32, RX = 4): 11 rows x
-// 2-3 LDS.128 per 4 points instead of 15 scalar LDS + address math per
-// point.  Needs every box row 16-byte aligned at the tile origin (the
-// per-array alignment shift sh == 0, true when the x loop starts at -ld_lo,
-// i.e. ghost width = stencil radius); otherwise the kernel takes the
-// per-point path.
-template <class NS, class T, int LAYOUT, int TX, int TY, int FORM, int RX>
+// A thread owns NY = TY/BY adjacent rows x RX adjacent x points of the tile.
+// Per march step it needs, for every static-load ROW of the body (the
+// lowering's row table: array + subscript offsets, innermost x aside) and
+// every one of its rows, a window of consecutive x elements.  The planner
+// (constexpr, per form) merges them into UNIQUE windows keyed by (array,
+// absolute y, march offset dz, other offsets) — the j+1 row of thread row 0
+// is the centre row of thread row 1 — and marks a window QUEUED when the
+// window one plane further along the march (dz + 1) covers its x range:
+// the value it needs at step s+1 is already in registers at step s.  Only
+// the rest is read from the staged TMA boxes, as 16-byte LDS.128 at
+// compile-time alignment (the tile origin is aligned down to V = 16/sizeof(T)
+// elements and every box starts RA below it).  jacobi7 (2 rows x 2 points per
+// thread): 3.5 doubles of shared memory per point instead of 7; wave4: the
+// k-2 / k-1 / k+1 planes of u come from the queue.
+//
+// Stores of arrays the nest never loads are deferred per point group and
+// written as one 16-byte STG per V points.
+struct UWin {
+    int arr = -1;
+    int off[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // x position 0, y position = absolute thread row offset
+    int xlo = 0, xhi = 0;
+    int src = -1;                             // queued: copied from this window at the end of a step
+    int dz = 0;
+};
+
+template <int MAXU, int MAXR, int NYM>
+struct UPlan {
+    UWin u[MAXU];
+    int n = 0;
+    int rmap[MAXR][NYM] = {};
+    int woff[MAXU + 1] = {};
+    int order[MAXU] = {};
+    bool ok = true;
+};
+
+template <class NS, class T, int LAYOUT, int TX, int TY, int BY, int FORM, int RX>
 struct WinPlan {
     using P = MarchPlan<NS, T, LAYOUT, TX, TY, RX>;
     static constexpr int V = 16 / (int)sizeof(T);
-    static constexpr int xpos(int a) {
+    static constexpr int NY = TY / BY;
+    static constexpr int RXV = RX / V;
+    static constexpr int MAXR = NS::NROW > 0 ? NS::NROW : 1;
+    static constexpr int MAXU = MAXR * NY;
+    static constexpr int pos_of(int a, int sg) {
         for (int p = 0; p < NS::ndim(a); ++p)
-            if (NS::ld_sig(a, p) == P::X) return p;
+            if (NS::ld_sig(a, p) == sg) return p;
         return -1;
     }
+    static constexpr int xpos(int a) { return pos_of(a, P::X); }
     static constexpr bool row_on(int r) {
-        return ((NS::row_forms(r) >> FORM) & 1) && P::staged(NS::row_arr(r)) && xpos(NS::row_arr(r)) >= 0;
+        return ((NS::row_forms(r) >> FORM) & 1) && P::staged(NS::row_arr(r)) && xpos(NS::row_arr(r)) >= 0 &&
+               !NS::is_int(NS::row_arr(r));
     }
-    static constexpr int width(int r) { return RX + NS::row_xhi(r) - NS::row_xlo(r); }
-    static constexpr int woff(int r) {
-        int o = 0;
-        for (int b = 0; b < r; ++b)
-            if (row_on(b)) o += width(b);
-        return o;
+    static constexpr UPlan<MAXU, MAXR, NY> build() {
+        UPlan<MAXU, MAXR, NY> pl{};
+        for (int r = 0; r < NS::NROW; ++r) {
+            if (!row_on(r)) continue;
+            const int a = NS::row_arr(r), xp = xpos(a), yp = pos_of(a, P::Y), mp = pos_of(a, 0);
+            for (int ry = 0; ry < NY; ++ry) {
+                int off[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int p = 0; p < NS::ndim(a); ++p)
+                    off[p] = p == xp ? 0 : (p == yp ? NS::row_off(r, p) + ry : NS::row_off(r, p));
+                int k = -1;
+                for (int j = 0; j < pl.n && k < 0; ++j) {
+                    bool same = pl.u[j].arr == a;
+                    for (int p = 0; p < 8; ++p) same = same && pl.u[j].off[p] == off[p];
+                    if (same) k = j;
+                }
+                if (k < 0) {
+                    if (pl.n >= MAXU) {
+                        pl.ok = false;
+                        return pl;
+                    }
+                    k = pl.n++;
+                    pl.u[k].arr = a;
+                    for (int p = 0; p < 8; ++p) pl.u[k].off[p] = off[p];
+                    pl.u[k].xlo = NS::row_xlo(r);
+                    pl.u[k].xhi = NS::row_xhi(r);
+                    pl.u[k].dz = mp >= 0 ? off[mp] : 0;
+                } else {
+                    if (NS::row_xlo(r) < pl.u[k].xlo) pl.u[k].xlo = NS::row_xlo(r);
+                    if (NS::row_xhi(r) > pl.u[k].xhi) pl.u[k].xhi = NS::row_xhi(r);
+                }
+                pl.rmap[r][ry] = k;
+            }
+        }
+        for (int k = 0; k < pl.n; ++k) {
+            const int a = pl.u[k].arr, mp = pos_of(a, 0);
+            if (mp < 0) continue;
+            for (int j = 0; j < pl.n; ++j) {
+                if (pl.u[j].arr != a || pl.u[j].off[mp] != pl.u[k].off[mp] + 1) continue;
+                bool same = true;
+                for (int p = 0; p < 8; ++p) same = same && (p == mp || pl.u[j].off[p] == pl.u[k].off[p]);
+                if (same && pl.u[j].xlo <= pl.u[k].xlo && pl.u[j].xhi >= pl.u[k].xhi) pl.u[k].src = j;
+            }
+        }
+        for (int k = 0; k < pl.n; ++k) pl.woff[k + 1] = pl.woff[k] + RX + pl.u[k].xhi - pl.u[k].xlo;
+        // queue copies in increasing dz: a source is read before it is overwritten
+        int m = 0;
+        for (int dz = -64; dz <= 64; ++dz)
+            for (int k = 0; k < pl.n; ++k)
+                if (pl.u[k].dz == dz) pl.order[m++] = k;
+        return pl;
     }
-    static constexpr int total() { return woff(NS::NROW); }
-    static constexpr int RXV = RX / V;
-    static constexpr int align(int r) {   // misalignment (elements) of the window start in its box row
-        const int a = NS::row_arr(r);
-        const int m = NS::row_xlo(r) - P::lo(a, xpos(a));
+    static constexpr UPlan<MAXU, MAXR, NY> PL = build();
+    // runtime-index accessors usable in device code (a local constant copy)
+    static __host__ __device__ constexpr int u_off(int k, int p) {
+        constexpr UPlan<MAXU, MAXR, NY> pl = build();
+        return pl.u[k].off[p];
+    }
+    static constexpr int total() { return PL.woff[PL.n]; }
+    static constexpr int width(int k) { return RX + PL.u[k].xhi - PL.u[k].xlo; }
+    static constexpr int align(int k) {   // misalignment (elements) of window k's start in its box row
+        const int m = PL.u[k].xlo - P::lo(PL.u[k].arr, xpos(PL.u[k].arr));
         return ((m % V) + V) % V;
     }
     template <int ARR, int... O>
@@ -362,19 +442,17 @@ struct WinPlan {
     }
     static constexpr bool usable() {
         if (RX <= 1) return false;
-        if (LAYOUT != 0 || RX % V != 0 || TX % RX != 0) return false;
-        for (int r = 0; r < NS::NROW; ++r)
-            if (row_on(r) && NS::is_int(NS::row_arr(r))) return false;
-        return total() > 0 && total() <= 160;
+        if (LAYOUT != 0 || RX % V != 0 || TX % RX != 0 || NS::NROW > 64) return false;
+        return PL.ok && total() > 0 && total() + NY * stotal() <= 192;
     }
 };
 
-// per-point view of the windows: point R0 of the thread's RX group
-template <class MM, class WP, class NS, int R0>
+// per-point view of the windows: point (RY, R0) of the thread's group
+template <class MM, class WP, class NS, int RY, int R0>
 struct WinMem {
     const MM& m;
     const typename MM::value_t* win;
-    typename MM::value_t* out;     // deferred stores of the point group
+    typename MM::value_t* out;     // deferred stores of this thread row
     bool defer;
     template <int ARR>
     using elem_t = typename MM::template elem_t<ARR>;
@@ -384,7 +462,9 @@ struct WinMem {
         if constexpr (r >= 0) {
             constexpr int off[sizeof...(O)] = {O...};
             constexpr int ox = off[WP::xpos(ARR)];
-            return win[WP::woff(r) + R0 + ox - NS::row_xlo(r)];
+            constexpr int k = WP::PL.rmap[r][RY];
+            constexpr int idx = WP::PL.woff[k] + R0 + ox - WP::PL.u[k].xlo;
+            return win[idx];
         } else {
             return m.template ld<ARR, O...>();
         }
@@ -453,7 +533,7 @@ __device__ __forceinline__ void march_issue(unsigned char* slot_base, const TmaM
 
 // TX x TY points per tile, BX x BY threads: each thread computes (TX/BX) x (TY/BY)
 // points per march step, amortising the step's barrier / mbarrier wait.
-template <class WP, class MM, class NS, int FORM, int R0, int RX>
+template <class WP, class MM, class NS, int FORM, int RY, int R0, int RX>
 __device__ __forceinline__ void win_run(MM& m, const typename MM::value_t* win, typename MM::value_t* out,
                                         bool defer, const KernelArgs<NS>& args, int* pt, int lx0, int xlo, int xhi) {
     if constexpr (R0 < RX) {
@@ -461,14 +541,14 @@ __device__ __forceinline__ void win_run(MM& m, const typename MM::value_t* win, 
         if (x < xhi && x >= xlo) {
             pt[NS::NLOOP - 1] = x;
             m.lx = lx0 + R0;
-            WinMem<MM, WP, NS, R0> wm{m, win, out, defer};
+            WinMem<MM, WP, NS, RY, R0> wm{m, win, out, defer};
             NS::template body<FORM>(wm, args.s, pt);
         }
-        win_run<WP, MM, NS, FORM, R0 + 1, RX>(m, win, out, defer, args, pt, lx0, xlo, xhi);
+        win_run<WP, MM, NS, FORM, RY, R0 + 1, RX>(m, win, out, defer, args, pt, lx0, xlo, xhi);
     }
 }
 
-// the group's deferred stores: one 16-byte vector store per V points
+// one thread row's deferred stores: one 16-byte vector store per V points
 template <class WP, class MM, class NS, int R>
 __device__ __forceinline__ void win_flush(const MM& m, const typename MM::value_t* out) {
     if constexpr (R < NS::NSROW) {
@@ -486,22 +566,67 @@ __device__ __forceinline__ void win_flush(const MM& m, const typename MM::value_
     }
 }
 
-template <class WP, class MM, class NS, int R>
-__device__ __forceinline__ void win_load(const MM& m, typename MM::value_t* win, int lx0) {
-    if constexpr (R < NS::NROW) {
-        if constexpr (WP::row_on(R)) {
+// unique window K from its staged box (skipped for queued windows after the
+// first step of a chunk: they were copied at the end of the previous step)
+template <class WP, class MM, class NS, int K>
+__device__ __forceinline__ void win_load(const MM& m, typename MM::value_t* win, int lx0, int ly0, bool first) {
+    if constexpr (K < WP::PL.n) {
+        constexpr bool queued = WP::PL.u[K].src >= 0;
+        constexpr int base = WP::PL.woff[K];
+        if (first || !queued) {
             using E = typename MM::value_t;
             using VT = typename Vec16<E>::type;
-            constexpr int V = WP::V, A = WP::align(R), W = WP::width(R);
+            constexpr int V = WP::V, A = WP::align(K), W = WP::width(K);
             constexpr int NV = (A + W + V - 1) / V;
-            const E* p = m.template row_ptr<R>(lx0) - A;
+            const E* p = m.template uwin_ptr<WP, K>(lx0, ly0) - A;
             E tmp[NV * V];
 #pragma unroll
             for (int v = 0; v < NV; ++v) *reinterpret_cast<VT*>(&tmp[v * V]) = *reinterpret_cast<const VT*>(p + v * V);
 #pragma unroll
-            for (int w = 0; w < W; ++w) win[WP::woff(R) + w] = tmp[A + w];
+            for (int w = 0; w < W; ++w) win[base + w] = tmp[A + w];
         }
-        win_load<WP, MM, NS, R + 1>(m, win, lx0);
+        win_load<WP, MM, NS, K + 1>(m, win, lx0, ly0, first);
+    }
+}
+
+// end of step: shift the queued windows one plane along the march
+template <class WP, class E, int I>
+__device__ __forceinline__ void win_shift(E* win) {
+    if constexpr (I < WP::PL.n) {
+        constexpr int K = WP::PL.order[I];
+        constexpr int S = WP::PL.u[K].src;
+        if constexpr (S >= 0) {
+            constexpr int dst = WP::PL.woff[K];
+            constexpr int src = WP::PL.woff[S] + WP::PL.u[K].xlo - WP::PL.u[S].xlo;
+            constexpr int W = WP::width(K);
+#pragma unroll
+            for (int w = 0; w < W; ++w) win[dst + w] = win[src + w];
+        }
+        win_shift<WP, E, I + 1>(win);
+    }
+}
+
+template <class WP, class M, class NS, int FORM, int RY, int RX, class T>
+__device__ __forceinline__ void win_rows(M& m, const T* win, bool vec_ok, const KernelArgs<NS>& args, int* pt,
+                                         int lx0, int ly0, int xlo0, int orgy) {
+    if constexpr (RY < WP::NY) {
+        using P = typename WP::P;
+        const int y = orgy + ly0 + RY;
+        if (NS::NLOOP < 3 || y < args.hi[1]) {
+            m.ly = ly0 + RY;
+            if constexpr (NS::NLOOP == 3) pt[1] = y;
+            T out[WP::stotal() > 0 ? WP::stotal() : 1];
+            const int x0 = m.orgx + lx0;
+            const bool defer = vec_ok && x0 >= xlo0 && x0 + RX <= args.hi[P::X];
+            win_run<WP, M, NS, FORM, RY, 0, RX>(m, win, out, defer, args, pt, lx0, xlo0, args.hi[P::X]);
+            if constexpr (WP::stotal() > 0) {
+                if (defer) {
+                    pt[P::X] = x0;
+                    win_flush<WP, M, NS, 0>(m, out);
+                }
+            }
+        }
+        win_rows<WP, M, NS, FORM, RY + 1, RX>(m, win, vec_ok, args, pt, lx0, ly0, xlo0, orgy);
     }
 }
 
@@ -558,7 +683,7 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
         m.sh[a] = xshift<P, NS>(a, orgx);
         if (P::staged(a) && m.sh[a] != 0) aligned = false;
     }
-    using WP = WinPlan<NS, T, LAYOUT, TX, TY, FORM, RX>;
+    using WP = WinPlan<NS, T, LAYOUT, TX, TY, BY, FORM, RX>;
     bool vec_ok = false;
     if constexpr (WP::usable()) {
         vec_ok = !args.sh.enabled;
@@ -574,6 +699,7 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
         }
     }
 
+    T win[WP::usable() ? WP::total() : 1];   // register windows, carried across steps (queue)
     for (int s = 0; s < ns; ++s) {
         __syncthreads();   // every thread is done with step s-1: its oldest slot is free
         if (tid == 0) {
@@ -592,25 +718,9 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
         m.newest = Bw % D;
         if constexpr (WP::usable()) {
             if (aligned) {
-#pragma unroll
-                for (int ry = 0; ry < TY / BY; ++ry) {
-                    m.ly = ty + ry * BY;
-                    const int y = orgy + m.ly;
-                    if (NS::NLOOP == 3 && y >= args.hi[1]) continue;
-                    if constexpr (NS::NLOOP == 3) pt[1] = y;
-                    T win[WP::total()];
-                    T out[WP::stotal() > 0 ? WP::stotal() : 1];
-                    win_load<WP, M, NS, 0>(m, win, tx * RX);
-                    const int x0 = orgx + tx * RX;
-                    const bool defer = vec_ok && x0 >= xlo0 && x0 + RX <= args.hi[P::X];
-                    win_run<WP, M, NS, FORM, 0, RX>(m, win, out, defer, args, pt, tx * RX, xlo0, args.hi[P::X]);
-                    if constexpr (WP::stotal() > 0) {
-                        if (defer) {
-                            pt[P::X] = x0;
-                            win_flush<WP, M, NS, 0>(m, out);
-                        }
-                    }
-                }
+                win_load<WP, M, NS, 0>(m, win, tx * RX, ty * WP::NY, s == 0);
+                win_rows<WP, M, NS, FORM, 0, RX>(m, win, vec_ok, args, pt, tx * RX, ty * WP::NY, xlo0, orgy);
+                win_shift<WP, T, 0>(win);
                 continue;
             }
         }
