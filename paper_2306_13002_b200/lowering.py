@@ -75,6 +75,7 @@ class Lowered:
     # component slices: independent groups of stores (and the statements
     # they need), each emitted as its own device body; [] = not sliceable
     slices: List[str] = field(default_factory=list)
+    slice_refs: List[list] = field(default_factory=list)   # per slice: sorted static load refs
     static_refs: set = field(default_factory=set)    # distinct (array, offsets) of static loads
     static_stores: set = field(default_factory=set)  # distinct (array, offsets) of static stores
 
@@ -138,6 +139,8 @@ class _Lowerer:
         self.body_stmt: Optional[ks.Stmt] = None
         self.static_refs: set = set()
         self.static_stores: set = set()
+        self.cur_refs: Optional[set] = None
+        self.slice_refs: List[list] = []
 
     # -- types
     def real(self) -> str:
@@ -338,6 +341,8 @@ class _Lowerer:
                 r[p][0] = min(r[p][0], o)
                 r[p][1] = max(r[p][1], o)
             self.static_refs.add((e.op, tuple(offs)))
+            if self.cur_refs is not None:
+                self.cur_refs.add((e.op, tuple(offs)))
             return f"m.template ld<{arr}, {', '.join(str(o) for o in offs)}>()"
         self.record_dynamic(e)
         self.n_dyn += 1
@@ -684,9 +689,21 @@ class _Lowerer:
             return None
         decls = [s_ for s_ in stmts if s_.kind == "decl"]
         out = []
+        import copy
         for root in sorted(groups, key=lambda r: min(order[x] for x in groups[r])):
             ids = sorted(groups[root], key=lambda x: order[x])
-            out.append(decls + [by_id[x] for x in ids])
+            body = [by_id[x] for x in ids]
+            used = set()
+            for st in body:
+                used |= ks_vars(st.rhs) | ks_vars(st.lhs)
+            kept = []
+            for d in decls:            # only the temps this slice touches
+                names = [nm for nm in d.names if nm[0] in used]
+                if names:
+                    d2 = copy.copy(d)
+                    d2.names = names
+                    kept.append(d2)
+            out.append(kept + body)
         return out
 
     def emit_slices(self) -> List[str]:
@@ -697,8 +714,11 @@ class _Lowerer:
         bodies = []
         for g in groups:
             out: List[str] = ["    " + x for x in self.pre]   # function-level locals (temp1, ...)
+            self.cur_refs = set()
             for st in g:
                 self.st(st, 2, out)
+            self.slice_refs.append(sorted(self.cur_refs))
+            self.cur_refs = None
             bodies.append("\n".join(out))
         self.n_fma, self.n_loads, self.n_dyn = saved
         return bodies
@@ -761,8 +781,8 @@ class _Lowerer:
         return Lowered(self.fn.name, self.fn.params, self.loop_vars, bounds,
                        {a: (s if s is not None else [-1] * len(self.arrays[a].dims)) for a, s in sig.items()},
                        self.stored, "\n".join(out), self.n_fma, self.n_loads, self.n_dyn, self.offrange,
-                       self.ldrange, self.dynrange, self.dynsig, self.loaded, must, slices, self.static_refs,
-                       self.static_stores)
+                       self.ldrange, self.dynrange, self.dynsig, self.loaded, must, slices, self.slice_refs,
+                       self.static_refs, self.static_stores)
 
 
 def lower_text(text: str, function: str, fma: bool, f32: bool = False, ifconv: bool = True) -> Lowered:
@@ -997,6 +1017,28 @@ def gen_function(nest: str, function: str, f32: bool = False) -> Tuple[str, dict
     soffs = [row(list(k[1])) for k in skeys] or [row([])]
     L.append(f"static __host__ __device__ constexpr int srow_off(int r, int p) {{ constexpr int t[{len(soffs)}][8] = {{"
              + ", ".join(soffs) + "}; return t[r][p]; }")
+    # per (form, slice): its static load refs (register queue of the sliced skeleton)
+    refl = []          # flattened (arr, offs)
+    start = []         # per form*MAXS + slice: first index
+    count = []
+    maxs = max(meta[f]["slices"] for f in forms)
+    for f in forms:
+        low = lows[f]
+        per = low.slice_refs if low.slices else [sorted(low.static_refs)]
+        for si in range(maxs):
+            refs = per[si] if si < len(per) else []
+            start.append(len(refl))
+            count.append(len(refs))
+            refl.extend(refs)
+    L.append(f"static constexpr int MAXSLICE = {maxs};")
+    L.append("static __host__ __device__ constexpr int sl_first(int f, int s) { constexpr int t[] = {"
+             + ", ".join(map(str, start)) + "}; return t[f * MAXSLICE + s]; }")
+    L.append("static __host__ __device__ constexpr int sl_nref(int f, int s) { constexpr int t[] = {"
+             + ", ".join(map(str, count)) + "}; return t[f * MAXSLICE + s]; }")
+    L.append("static __host__ __device__ constexpr int sl_arr(int i) { constexpr int t[] = {"
+             + (", ".join(str(names.index(a)) for a, _ in refl) or "0") + "}; return t[i]; }")
+    L.append("static __host__ __device__ constexpr int sl_off(int i, int p) { constexpr int t[][8] = {"
+             + (", ".join(row(list(o)) for _, o in refl) or row([])) + "}; return t[i][p]; }")
     L.append("static constexpr bool has_dynamic_index = " + ("true" if any(m_["dyn_loads"] for m_ in meta.values()) else "false") + ";")
     args = ", ".join(f"pt[{d}]" for d in range(len(base.loop_vars)))
     L.append("// component slices per acs_variant (1 = the whole body)")
