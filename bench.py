@@ -202,7 +202,29 @@ def bench_kernel(kid, size, dtype, sweeps, variant, schedule, reps=5, warmup=3):
             k.launch(a, sc, variant, schedule, stream)
             state["t"] = t + 1
 
-    ms = time_steps(step, reps, warmup, stream)
+    run = step
+    if sweeps > 1 and sweeps % 2 == 0 and w.spec.nest != "wave4":
+        # a multi-sweep step (Jacobi: 100 ping-pong sweeps) is one CUDA graph
+        # of `sweeps` kernel launches, captured once and replayed: the
+        # per-launch host cost leaves the timed region, as in a real time loop
+        for _ in range(warmup):
+            step()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        with torch.cuda.graph(g, stream=cs):
+            for _ in range(sweeps):
+                a = dict(arrs)
+                t = state["t"]
+                if pair and t % 2 == 1:
+                    a[pair[0]], a[pair[1]] = arrs[pair[1]], arrs[pair[0]]
+                k.launch(a, sc, variant, schedule, cs)
+                state["t"] = t + 1
+        stream.wait_stream(cs)
+        torch.cuda.synchronize()
+        run = lambda: g.replay()  # noqa: E731
+    ms = time_steps(run, reps, warmup, stream)
     gbs = w.algorithmic_bytes * sweeps / (ms * 1e-3) / 1e9
     del arrs
     torch.cuda.empty_cache()
@@ -443,6 +465,8 @@ def per_kernel_table(peak):
     for kid, size, dtype, sweeps in TABLE:
         fn = kid.split(":")[1]
         row = {"size": size, "dtype": dtype, "sweeps_per_step": sweeps}
+        if sweeps > 1:
+            row["launch"] = f"CUDA graph of {sweeps} kernel launches per step (every form alike)"
         try:
             slot, name, tms = tune_kernel(kid, size, dtype, "accsat")
             row["tuned"] = {"slot": slot, "schedule": name, "ms_per_slot": {str(s): round(v, 4) for s, v in tms.items()}}
