@@ -237,6 +237,22 @@ class HostRunner:
                     self.launches += 1
         cur.wait_stream(self.s_d2h)
 
+    def capture(self, scalars: Dict[str, float], variant: str = "accsat", schedule="default"):
+        """The whole call (every chunk's H2D, remap, launch, remap, D2H on the
+        three streams) captured once as a CUDA graph; replay() re-runs it on
+        the current host buffers with no per-chunk host work."""
+        torch = self.torch
+        self.run(scalars, variant, schedule)           # warm: plans, attributes, tensor maps
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(g, stream=cs):
+            self.run(scalars, variant, schedule)
+        torch.cuda.current_stream().wait_stream(cs)
+        torch.cuda.synchronize()
+        return g
+
     def bytes_per_call(self):
         h2d = d2h = 0
         for name, r in self.reach.items():

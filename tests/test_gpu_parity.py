@@ -257,3 +257,28 @@ def test_host_runner_overlapped_equals_oracle(kid, size, dtype, chunks):
     torch.cuda.synchronize()
     for n in ins2:
         assert bitwise_equal(host[n].numpy(), want2[n]), f"{kid} chunks={chunks} (second call): '{n}'"
+
+
+@pytest.mark.parametrize("kid,size,dtype", [("d3q19.c:stream_collide:0", (13, 9, 20), "f64"),
+                                            ("wave4.c:wave4:0", (17, 8, 33), "f32")])
+def test_host_runner_graph_replay_equals_oracle(kid, size, dtype):
+    """The host-buffer call captured as a CUDA graph: replaying it on new host
+    inputs (same buffers) gives the oracle's result for those inputs."""
+    torch = _torch()
+    from paper_2306_13002_b200 import pipeline_exec
+    spec = nests.kernel(kid)
+    w = nests.workload(kid, size, dtype=dtype)
+    ins = nests.make_inputs(w)
+    host = {n: torch.from_numpy(a.copy()).pin_memory() for n, a in ins.items()}
+    k = backend.Kernel.lookup(kid)
+    r = pipeline_exec.HostRunner(k, host, spec.range_params, chunks=3)
+    g = r.capture(dict(w.scalars), "accsat")
+    ins2 = {n: (a * a.dtype.type(0.5) if a.dtype.kind == "f" else a.copy()) for n, a in ins.items()}
+    want = {n: a.copy() for n, a in ins2.items()}
+    oracle_cpu.run(spec, want, w.scalars, "accsat", fma=True, f32=dtype == "f32")
+    for n in ins2:
+        host[n].copy_(torch.from_numpy(ins2[n]))
+    g.replay()
+    torch.cuda.synchronize()
+    for n in ins2:
+        assert bitwise_equal(host[n].numpy(), want[n]), f"{kid} graph replay: '{n}'"
