@@ -481,7 +481,8 @@ def per_kernel_table(peak):
             row["tuned"] = {"slot": slot, "schedule": name, "ms_per_slot": {str(s): round(v, 4) for s, v in tms.items()}}
         except Exception as e:
             row["tuned"] = {"error": str(e)[:200]}
-        for variant, sched in (("original", "naive"), ("accsat", "naive"), ("accsat", "default")):
+        for variant, sched in (("original", "naive"), ("original-nvcc", "naive"), ("accsat", "naive"),
+                               ("accsat", "default")):
             try:
                 ms, gbs, w = bench_kernel(kid, size, dtype, sweeps, variant, sched, reps=3 if sweeps > 1 else 5)
                 row[f"{variant}/{sched}"] = {"ms": round(ms, 4), "gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
@@ -489,6 +490,7 @@ def per_kernel_table(peak):
                 row[f"{variant}/{sched}"] = {"error": str(e)[:200]}
         try:
             row["sat_vs_orig_speedup"] = round(row["accsat/default"]["gbs"] / row["original/naive"]["gbs"], 3)
+            row["sat_vs_nvcc_default_speedup"] = round(row["accsat/default"]["gbs"] / row["original-nvcc/naive"]["gbs"], 3)
             row["bytes_per_point"] = w.bytes_per_point
         except Exception:
             pass

@@ -58,7 +58,14 @@ typedef enum {
     ACS_CSE = 1,
     ACS_CSE_BULK = 2,
     ACS_CSE_SAT = 3,
-    ACS_ACCSAT = 4
+    ACS_ACCSAT = 4,
+    /* Measurement baseline, not a reference form: the ORIGINAL text compiled
+     * the way nvcc does by default (plain C arithmetic with FMA contraction
+     * left to the compiler, loads free to be cached / CSE'd) — how much of the
+     * saturation win a production compiler recovers on its own (SURVEY.md §7
+     * hard part 1).  Naive schedule only; results agree with the reference
+     * within the comparator tolerance, not bit for bit. */
+    ACS_ORIGINAL_NVCC = 5
 } acs_variant;
 
 /* Kernel skeleton: NAIVE = one thread per point, every array reference of the

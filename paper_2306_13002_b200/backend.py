@@ -30,7 +30,8 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "accsat_b200.h")
 
 ACS_OK, ACS_E_ARG, ACS_E_NO_KERNEL, ACS_E_SHAPE, ACS_E_CUDA, ACS_E_NCCL, ACS_E_BOUNDS = range(7)
 F64, F32, I32, I64, U8 = range(5)
-VARIANTS = {"original": 0, "cse": 1, "cse+bulk": 2, "cse+sat": 3, "accsat": 4}
+VARIANTS = {"original": 0, "cse": 1, "cse+bulk": 2, "cse+sat": 3, "accsat": 4,
+            "original-nvcc": 5}   # measurement baseline: original text, nvcc-default arithmetic
 SCHEDULES = {"default": 0, "naive": 1, "tiled": 2}
 FILL = {"uniform": 0, "const": 1, "mask": 2, "d3q19": 3}
 MAX_DIMS = 8

@@ -399,14 +399,14 @@ static acs_status launch_impl(const acs_kernel* k, acs_variant variant, acs_sche
         return ACS_E_ARG;
     }
     const Entry* e = reinterpret_cast<const Entry*>(k);
-    if ((int)variant < 0 || (int)variant > 4) {
+    if ((int)variant < 0 || (int)variant > 5) {
         set_error("acs_launch: unknown variant");
         return ACS_E_ARG;
     }
     const int prec = precision_of(arrays, n_arrays);
     int slot;
     if (schedule == ACS_SCHED_DEFAULT)
-        slot = variant == ACS_ORIGINAL ? 0 : e->best[prec][variant];
+        slot = (variant == ACS_ORIGINAL || variant == ACS_ORIGINAL_NVCC) ? 0 : e->best[prec][variant];
     else if (schedule == ACS_SCHED_NAIVE)
         slot = 0;
     else if (schedule == ACS_SCHED_TILED)

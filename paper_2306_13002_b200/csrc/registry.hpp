@@ -42,10 +42,10 @@ struct Entry {
     std::vector<int> scalar_is_int;
     int static_loads[5] = {0, 0, 0, 0, 0};
     int fma_count[5] = {0, 0, 0, 0, 0};
-    LaunchFn launch[2][5][kMaxSched] = {};
+    LaunchFn launch[2][6][kMaxSched] = {};   // variant 5 = ACS_ORIGINAL_NVCC (naive slot only)
     std::string sched_name[2][kMaxSched];
     int n_sched[2] = {1, 1};     // slot 0 (naive) always present once registered
-    int best[2][5] = {};         // preferred slot per (precision, variant); acs_tune updates it
+    int best[2][6] = {};         // preferred slot per (precision, variant); acs_tune updates it
     bool soa_last_dim = false;   // backend layout: trailing component subscript made slowest (D3Q19 q)
     std::vector<int> component_last;  // per array: trailing subscript is an absolute component index
     struct Reach {
@@ -214,6 +214,7 @@ void fill_naive(Entry& e, int prec) {
     e.launch[prec][2][0] = &launch_naive<NS, T, 2>;
     e.launch[prec][3][0] = &launch_naive<NS, T, 3>;
     e.launch[prec][4][0] = &launch_naive<NS, T, 4>;
+    e.launch[prec][5][0] = &launch_naive<NS, T, 5>;
     e.sched_name[prec][0] = "naive (one thread per point, as-written loads for ORIGINAL)";
 }
 

@@ -105,7 +105,8 @@ def _affine_expr(var: Optional[str], off: int) -> ks.Expr:
 
 
 class _Lowerer:
-    def __init__(self, fn: ks.Function, region: ks.Region, fma: bool, f32: bool, ifconv: bool = True):
+    def __init__(self, fn: ks.Function, region: ks.Region, fma: bool, f32: bool, ifconv: bool = True,
+                 plain: bool = False):
         self.fn = fn
         self.region = region
         self.fma = fma
@@ -136,6 +137,7 @@ class _Lowerer:
         self.capture: Optional[Dict[tuple, str]] = None   # if-conversion: store target -> value var
         self.n_ifc = 0
         self.ifconv = ifconv
+        self.plain = plain      # nvcc-default arithmetic: C operators, contraction left to the compiler
         self.body_stmt: Optional[ks.Stmt] = None
         self.static_refs: set = set()
         self.static_stores: set = set()
@@ -257,6 +259,8 @@ class _Lowerer:
             return f"(({a}) {op} ({b}))", "int"
         if op == "%":
             raise LowerError("'%' requires integer operands")
+        if self.plain:
+            return f"(({a}) {op} ({b}))", "double"
         sfx = "f" if self.f32 else "d"
         name = {"+": "add", "-": "sub", "*": "mul", "/": "div"}[op]
         return f"__{sfx}{name}_rn({a}, {b})", "double"
@@ -266,6 +270,8 @@ class _Lowerer:
         n = e.op
         f = "f" if self.f32 else ""
         if n == "sqrt":
+            if self.plain:
+                return f"sqrt{f}({args[0]})"
             return f"__{'f' if self.f32 else 'd'}sqrt_rn({args[0]})"
         if n in LIBM1 and len(args) == 1:
             return f"{n}{f}({args[0]})"
@@ -785,11 +791,12 @@ class _Lowerer:
                        self.static_refs, self.static_stores)
 
 
-def lower_text(text: str, function: str, fma: bool, f32: bool = False, ifconv: bool = True) -> Lowered:
+def lower_text(text: str, function: str, fma: bool, f32: bool = False, ifconv: bool = True,
+               plain: bool = False) -> Lowered:
     mod = ks.parse(text)
     for reg in ks.find_regions(mod):
         if reg.function.name == function:
-            return _Lowerer(reg.function, reg, fma, f32, ifconv).run()
+            return _Lowerer(reg.function, reg, fma, f32, ifconv, plain).run()
     raise LowerError(f"no region in function {function}")
 
 
@@ -870,6 +877,19 @@ def gen_function(nest: str, function: str, f32: bool = False) -> Tuple[str, dict
         L.append(f"    lo[{d}] = {lo}; hi[{d}] = {hi};")
     L.append("}")
     meta = {}
+    # measurement baseline (acs_variant 5, ACS_ORIGINAL_NVCC): the original text
+    # as nvcc compiles it by default — C operators with FMA contraction left to
+    # the compiler, loads free to be cached/CSE'd.  Not bit-exact by design.
+    nv = lower_text(texts["original"][0], function, False, f32, plain=True)
+    lvn = ", ".join(f"const int {v}" for v in nv.loop_vars)
+    L.append("// form original_nvcc: the original text, nvcc-default arithmetic (contraction allowed)")
+    L.append("template <class M>")
+    L.append(f"static __device__ __forceinline__ void body_original_nvcc(M& m, const Scalars& s_, {lvn}) {{")
+    for p in sc:
+        ty = "int" if p.ty == "int" else ("float" if f32 else "double")
+        L.append(f"    {ty} {p.name} = s_.{p.name}; (void){p.name};")
+    L.append(nv.body)
+    L.append("}")
     for form, low in lows.items():
         lv = ", ".join(f"const int {v}" for v in low.loop_vars)
         L.append(f"// form {form}: {low.n_loads} static loads ({low.n_dyn_loads} data-dependent), "
@@ -1054,6 +1074,7 @@ def gen_function(nest: str, function: str, f32: bool = False) -> Tuple[str, dict
     for fi, f in enumerate(forms):
         kw = "if" if fi == 0 else "else if"
         L.append(f"    {kw} constexpr (FORM == {fi}) body_{f}(m, s, {args});")
+    L.append(f"    else if constexpr (FORM == 5) body_original_nvcc(m, s, {args});")
     L.append("}")
     L.append(f"}};  // struct {ns}")
     return "\n".join(L) + "\n", meta

@@ -282,3 +282,25 @@ def test_host_runner_graph_replay_equals_oracle(kid, size, dtype):
     torch.cuda.synchronize()
     for n in ins2:
         assert bitwise_equal(host[n].numpy(), want[n]), f"{kid} graph replay: '{n}'"
+
+
+@pytest.mark.parametrize("kid,size", cases(), ids=[f"{k.split(':')[1]}-{s}" for k, s in cases()])
+def test_original_nvcc_default_within_tolerance(kid, size):
+    """ACS_ORIGINAL_NVCC (measurement baseline: the original text with nvcc's
+    default contraction) agrees with the reference's two-rounding original
+    within rel 1e-12 or a norm-wise floor 1e-12 * max|ref|."""
+    spec = nests.kernel(kid)
+    w = nests.workload(kid, size)
+    ins = nests.make_inputs(w)
+    want = {n: a.copy() for n, a in ins.items()}
+    oracle_cpu.run(spec, want, w.scalars, "original")
+    got = run_gpu(kid, ins, w.scalars, "original-nvcc", 0)
+    for n in w.write_arrays:
+        a, b = got[n].astype(np.float64), want[n].astype(np.float64)
+        if got[n].dtype.kind != "f":
+            assert np.array_equal(a, b), f"{kid} original-nvcc: integer array '{n}' differs"
+            continue
+        d = np.abs(a - b)
+        floor = 1e-12 * np.max(np.abs(b)) if b.size else 0.0
+        ok = (d <= 1e-12 * np.maximum(np.abs(a), np.abs(b))) | (d <= floor)
+        assert np.all(ok), f"{kid} original-nvcc size={size}: '{n}' max abs {np.max(d)}"
