@@ -137,6 +137,10 @@ struct NaiveMem {
     __device__ __forceinline__ elem_t<ARR> ld() const { return load_at<ARR>(static_index<ARR, O...>()); }
     template <int ARR, class... I>
     __device__ __forceinline__ elem_t<ARR> ldx(I... idx) const { return load_at<ARR>(dyn_index<ARR>(idx...)); }
+    // data-dependent index the lowering proved to lie in the load's value set
+    // (every candidate affine in the loop variables): same element as ldx
+    template <int ARR, class... I>
+    __device__ __forceinline__ elem_t<ARR> ldx_in(I... idx) const { return ldx<ARR>(idx...); }
     // write-through of a store to the neighbours that hold plane l0 (sharded launches)
     template <int ARR>
     __device__ __forceinline__ void forward(long long idx, long long l0, elem_t<ARR> v) const {

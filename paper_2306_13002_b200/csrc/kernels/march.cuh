@@ -235,6 +235,32 @@ struct MarchMem {
         return reinterpret_cast<const T*>(box_base<A>(delta)) + idx;
     }
 
+    // a data-dependent index whose every candidate value is affine in the loop
+    // variables (the lowering's value-set proof): the staged box was sized to
+    // hold all of them, so no range check and no global fallback
+    template <int ARR, class... I>
+    __device__ __forceinline__ elem_t<ARR> ldx_in(I... ii) const {
+        if constexpr (P::staged(ARR)) {
+            const int v[sizeof...(I)] = {(int)ii...};
+            int idx = 0, delta = 0;
+#pragma unroll
+            for (int p = 0; p < (int)sizeof...(I); ++p) {
+                const int s = NS::ld_sig(ARR, p);
+                const int lo = P::lo(ARR, p);
+                if (s == 0) {
+                    delta = D + (v[p] - k) - NS::ld_hi(ARR, p);
+                } else {
+                    const int l = v[p] - lo - (s == P::X ? orgx : (s == P::Y ? orgy : 0));
+                    idx += (l + (s == P::X ? sh[ARR] : 0)) * P::bstride(ARR, p);
+                }
+            }
+            if (delta >= D) delta -= D;
+            return box_base<ARR>(delta)[idx];
+        } else {
+            return g.template ldx<ARR>(ii...);
+        }
+    }
+
     // out-of-box dynamic index: rare (e.g. advec's clamp at the domain edge),
     // kept out of line so the in-box path stays a few integer ops + one LDS
     template <int ARR, class... I>
@@ -471,6 +497,8 @@ struct WinMem {
     }
     template <int ARR, class... I>
     __device__ __forceinline__ elem_t<ARR> ldx(I... ii) const { return m.template ldx<ARR>(ii...); }
+    template <int ARR, class... I>
+    __device__ __forceinline__ elem_t<ARR> ldx_in(I... ii) const { return m.template ldx_in<ARR>(ii...); }
     template <int ARR, int... O>
     __device__ __forceinline__ void st(elem_t<ARR> v) const {
         constexpr int r = WP::template srow_of<ARR, O...>();

@@ -132,6 +132,8 @@ struct QMem {
     }
     template <int ARR, class... I>
     __device__ __forceinline__ elem_t<ARR> ldx(I... ii) const { return g.template ldx<ARR>(ii...); }
+    template <int ARR, class... I>
+    __device__ __forceinline__ elem_t<ARR> ldx_in(I... ii) const { return g.template ldx<ARR>(ii...); }
     template <int ARR, int... O>
     __device__ __forceinline__ void st(elem_t<ARR> v) const { g.template st<ARR, O...>(v); }
     template <int ARR, class... A>

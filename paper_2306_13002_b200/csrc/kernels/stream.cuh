@@ -100,6 +100,8 @@ struct StreamMem {
     }
     template <int ARR, class... I>
     __device__ __forceinline__ elem_t<ARR> ldx(I... idx) const { return g.template ldx<ARR>(idx...); }
+    template <int ARR, class... I>
+    __device__ __forceinline__ elem_t<ARR> ldx_in(I... idx) const { return g.template ldx<ARR>(idx...); }
     template <int ARR, int... O>
     __device__ __forceinline__ void st(elem_t<ARR> v) const { g.template st<ARR, O...>(v); }
     template <int ARR, class... A>

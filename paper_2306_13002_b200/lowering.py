@@ -353,7 +353,15 @@ class _Lowerer:
         self.record_dynamic(e)
         self.n_dyn += 1
         idx = ", ".join(self.conv(*self.ex(i), "int") for i in e.kids)
-        return f"m.template ldx<{arr}>({idx})"
+        # every candidate value of every subscript affine in ONE loop variable
+        # (or constant): the tiled skeletons size their staged box to hold all
+        # of them, so the element needs no range check (ldx_in)
+        safe = True
+        for i in e.kids:
+            vals = self.value_set(i)
+            if any(v is None for v in vals) or len({v.var for v in vals}) != 1:
+                safe = False
+        return f"m.template {'ldx_in' if safe else 'ldx'}<{arr}>({idx})"
 
     # -- statements
     def is_fma_temp(self, s: ks.Stmt) -> Optional[Tuple[ks.Expr, ks.Expr, ks.Expr]]:

@@ -158,3 +158,13 @@ def test_generated_headers_are_current(tmp_path):
         want = open(os.path.join(tmp_path, f)).read()
         have = open(os.path.join(ROOT, "paper_2306_13002_b200", "csrc", "gen", f)).read()
         assert have == want, f"{f} is stale: re-run python -m paper_2306_13002_b200.lowering"
+
+
+def test_value_set_proven_dynamic_loads():
+    """advec: donor / downwind take only affine candidates (j-1 or j) -> ldx_in
+    (no range check); upwind can be the clamp nx-1 (not affine in j) -> ldx."""
+    low = lower(emitted("clover", "accsat"), "advec_cell_x")
+    assert re.search(r"ldx_in<ARR_density1>\(k, donor\)", low.body)
+    assert re.search(r"ldx_in<ARR_pre_vol>\(k, donor\)", low.body)
+    assert re.search(r"ldx<ARR_density1>\(k, upwind\)", low.body)
+    assert not re.search(r"ldx_in<ARR_density1>\(k, upwind\)", low.body)
