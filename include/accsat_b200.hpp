@@ -80,7 +80,14 @@ class InternalError : public std::logic_error {
 };
 
 // VariantConfig names (cse, cse+sat, cse+bulk, accsat) plus the original text.
-enum class Variant { Original = ACS_ORIGINAL, Cse = ACS_CSE, CseBulk = ACS_CSE_BULK, CseSat = ACS_CSE_SAT, AccSat = ACS_ACCSAT };
+enum class Variant {
+    Original = ACS_ORIGINAL,
+    Cse = ACS_CSE,
+    CseBulk = ACS_CSE_BULK,
+    CseSat = ACS_CSE_SAT,
+    AccSat = ACS_ACCSAT,
+    OriginalNvcc = ACS_ORIGINAL_NVCC   // measurement baseline, not a reference form
+};
 
 inline Variant variant_from_name(const std::string& s) {
     if (s == "original") return Variant::Original;
@@ -88,6 +95,7 @@ inline Variant variant_from_name(const std::string& s) {
     if (s == "cse+bulk") return Variant::CseBulk;
     if (s == "cse+sat") return Variant::CseSat;
     if (s == "accsat") return Variant::AccSat;
+    if (s == "original-nvcc") return Variant::OriginalNvcc;
     throw std::invalid_argument("unknown variant: " + s + " (expected original, cse, cse+sat, cse+bulk, or accsat)");
 }
 

@@ -82,3 +82,14 @@ def test_launch_without_gpu_fails_loudly():
     env = backend.Environment({}, {})
     with pytest.raises(backend.InternalError):
         backend.eval_region("jacobi7.c:jacobi7:0", env)
+
+
+def test_cpp_host_api_compiles():
+    """include/accsat_b200.hpp (the C++ mirror of the reference's eval_region /
+    Environment / diff_test types) compiles as a satcc call site would use it."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-I", os.path.join(root, "include"),
+                        "-I", "/usr/local/cuda/include", os.path.join(root, "tests", "cpp", "host_api_check.cpp")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

@@ -304,3 +304,16 @@ def test_original_nvcc_default_within_tolerance(kid, size):
         floor = 1e-12 * np.max(np.abs(b)) if b.size else 0.0
         ok = (d <= 1e-12 * np.maximum(np.abs(a), np.abs(b))) | (d <= floor)
         assert np.all(ok), f"{kid} original-nvcc size={size}: '{n}' max abs {np.max(d)}"
+
+
+def test_cpp_host_api_on_gpu():
+    """The C++ host API end to end (tests/cpp/host_api_check.cpp): eval_region
+    of jacobi7 original + accsat bit-exact vs a C++ restatement, comparator
+    rule, EvalError on a missing array."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "build", "host_api_check")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", os.path.join(root, "tests", "cpp")], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "host_api_check ok" in r.stdout, r.stdout + r.stderr
