@@ -246,6 +246,7 @@ def main():
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--e2e-eager", action="store_true", help="enqueue the e2e call eagerly instead of a CUDA graph")
+    ap.add_argument("--e2e-ramp", action="store_true", help="smaller first/last chunks in the e2e pipeline (measured: no gain)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -441,7 +442,7 @@ def e2e_d3q19(args, w, k, dist):
         host[n].copy_(t)
     del dev_rm
     torch.cuda.synchronize()
-    runner = pipeline_exec.HostRunner(k, host, w.spec.range_params, chunks=args.e2e_chunks)
+    runner = pipeline_exec.HostRunner(k, host, w.spec.range_params, chunks=args.e2e_chunks, ramp=args.e2e_ramp)
     sc = dict(w.scalars)
 
     def step():

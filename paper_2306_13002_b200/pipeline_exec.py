@@ -113,13 +113,15 @@ class HostRunner:
     """Reusable device buffers + streams for repeated host-buffer calls of one
     kernel on one problem shape."""
 
-    def __init__(self, k: backend.Kernel, host: Dict[str, object], range_params, chunks: int = 8):
+    def __init__(self, k: backend.Kernel, host: Dict[str, object], range_params, chunks: int = 8,
+                 ramp: bool = False):
         import torch
         self.torch = torch
         self.k = k
         self.host = host
         self.rp = range_params
         self.chunks = chunks
+        self.ramp = ramp
         self.reach = reaches(k)
         self.rm = {n: torch.empty(tuple(t.shape), dtype=t.dtype, device="cuda") for n, t in host.items()}
         self.nat = {n: backend.empty_native(k, n, tuple(t.shape), t.dtype) for n, t in host.items()}
@@ -127,6 +129,28 @@ class HostRunner:
         self.launches = 0
         self.shell: Dict[str, List] = {}      # store-only arrays: boxes outside the write core
         self._shell_key = None
+
+    def _cuts(self, b: int, n: int) -> List[int]:
+        """Chunk boundaries of the outermost loop.  With `ramp`, the first and
+        last chunks are smaller (1/4, 1/2 of the rest): the download can start
+        sooner and the final download after the last kernel is shorter."""
+        C = self.chunks
+        if not self.ramp or C < 6:
+            return [b + n * c // C for c in range(C + 1)]
+        w = [1.0] * C
+        w[0] = w[-1] = 0.25
+        w[1] = w[-2] = 0.5
+        tot = sum(w)
+        cuts, acc = [b], 0.0
+        for c in range(C):
+            acc += w[c]
+            cuts.append(b + int(round(n * acc / tot)))
+        cuts[-1] = b + n
+        out = [cuts[0]]
+        for x in cuts[1:]:
+            if x > out[-1]:
+                out.append(x)
+        return out
 
     def _plan_shells(self, scalars):
         key = tuple(sorted((n, float(v)) for n, v in scalars.items()))
@@ -168,7 +192,8 @@ class HostRunner:
         beg, end = self.rp
         b, e = int(scalars[beg]), int(scalars[end])
         n = e - b
-        cuts = [b + n * c // self.chunks for c in range(self.chunks + 1)]
+        cuts = self._cuts(b, n)
+        nch = len(cuts) - 1
         cur = torch.cuda.current_stream()
         for s in (self.s_h2d, self.s_cmp, self.s_d2h):
             s.wait_stream(cur)
@@ -180,7 +205,7 @@ class HostRunner:
         uploaded = {nm: -10**9 for nm in self.host}       # highest plane uploaded so far (exclusive)
         downloaded = {nm: -10**9 for nm in self.host}
         first = True
-        for c in range(self.chunks):
+        for c in range(nch):
             p0, p1 = cuts[c], cuts[c + 1]
             remap_in = []
             for name, r in self.reach.items():
@@ -190,7 +215,7 @@ class HostRunner:
                 hi = p1 + max(r.ld_hi if r.loaded else 0, r.st_hi if r.stored else 0)
                 if c == 0:
                     lo = min(lo, 0)                      # planes below the loop range: copied once
-                if c == self.chunks - 1:
+                if c == nch - 1:
                     hi = max(hi, self.host[name].shape[0])
                 lo = max(lo, uploaded[name])
                 lo, hi = self._clip(lo, hi, self.host[name].shape[0])
@@ -216,14 +241,14 @@ class HostRunner:
             for name, r in self.reach.items():
                 if not (r.sliced and r.stored):
                     continue
-                final_hi = cuts[c + 1] + r.st_lo if c + 1 < self.chunks else self.host[name].shape[0]
+                final_hi = cuts[c + 1] + r.st_lo if c + 1 < nch else self.host[name].shape[0]
                 lo = 0 if c == 0 else downloaded[name]
                 lo, hi = self._clip(lo, final_hi, self.host[name].shape[0])
                 if hi > lo:
                     backend.copy(self.rm[name][lo:hi], self.nat[name][lo:hi], self.s_cmp)
                     out.append((name, lo, hi))
                 downloaded[name] = max(downloaded[name], final_hi)
-            if c == self.chunks - 1:
+            if c == nch - 1:
                 for name, r in self.reach.items():
                     if not r.sliced and r.stored:
                         backend.copy(self.rm[name], self.nat[name], self.s_cmp)
