@@ -7,12 +7,17 @@
 // 25-component boxes of both jacobians per k-plane through TMA; the sliced
 // skeleton gives each of the 25 independent (m, n) components its own
 // threads, marching k with the re-reads served by L1.
+//
+// The sliced configurations are instantiated in their own translation units
+// (nest_zsolve_s*.cu) so nvcc compiles them in parallel.
 #include "registry.hpp"
-#include "kernels/march.cuh"
-#include "kernels/sliced.cuh"
 #include "gen/zsolve.cuh"
 
 namespace acs {
+
+void fill_zsolve_sliced_a(Entry& e);
+void fill_zsolve_sliced_b(Entry& e);
+void fill_zsolve_sliced_c(Entry& e);
 
 void register_zsolve() {
     static Entry e;
@@ -20,9 +25,9 @@ void register_zsolve() {
     e.function = "z_solve_lhs";
     describe<gen::z_solve_lhs>(e, "zsolve.c", 0);
     fill_naive<gen::z_solve_lhs, double>(e, 0);
-    fill_sliced<gen::z_solve_lhs, double, 128, 2, 32>(e, 0);
-    fill_sliced<gen::z_solve_lhs, double, 64, 4, 16>(e, 0);
-    fill_sliced<gen::z_solve_lhs, double, 128, 1, 64>(e, 0);
+    fill_zsolve_sliced_a(e);
+    fill_zsolve_sliced_b(e);
+    fill_zsolve_sliced_c(e);
     register_entry(&e);
 }
 

@@ -1,0 +1,10 @@
+// zsolve sliced configuration (128 x 2, k-chunk 32), own translation unit.
+#include "registry.hpp"
+#include "kernels/sliced.cuh"
+#include "gen/zsolve.cuh"
+
+namespace acs {
+
+void fill_zsolve_sliced_a(Entry& e) { fill_sliced<gen::z_solve_lhs, double, 128, 2, 32>(e, 0); }
+
+}  // namespace acs
