@@ -317,3 +317,67 @@ def test_cpp_host_api_on_gpu():
         subprocess.run(["make", "-s", "-C", os.path.join(root, "tests", "cpp")], check=True)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "host_api_check ok" in r.stdout, r.stdout + r.stderr
+
+
+# ---- edge cases: empty iteration spaces ---------------------------------------
+
+@pytest.mark.parametrize("kid", sorted(nests.KERNELS))
+@pytest.mark.parametrize("which", ["outer", "inner"])
+def test_empty_iteration_space_is_a_noop(kid, which):
+    """A nest whose loop range is empty (kbeg == kend, or no interior rows)
+    runs no point: every array keeps its input bits, in every form and
+    schedule slot (the interpreter executes zero iterations)."""
+    spec = nests.kernel(kid)
+    dtype = "f32" if spec.nest == "wave4" else "f64"
+    w = nests.workload(kid, {3: (4, 5, 9), 2: (6, 9)}[len(spec.loop_vars)], dtype=dtype)
+    sc = dict(w.scalars)
+    beg, end = spec.range_params
+    if which == "outer":
+        sc[end] = sc[beg]
+    else:
+        key = "ny" if "ny" in sc and len(spec.loop_vars) == 3 else "nx"
+        sc[key] = 1             # every inner loop bound (n - 1, n - 2) is then empty
+    ins = nests.make_inputs(w)
+    for variant in VARIANTS:
+        for sched in schedules(kid, prec=1 if dtype == "f32" else 0):
+            got = run_gpu(kid, ins, sc, variant, sched)
+            for n in ins:
+                assert bitwise_equal(got[n], ins[n]), f"{kid} {variant}/{sched} empty {which}: '{n}' changed"
+
+
+# ---- full BASELINE sizes: the GPU against the compiled reference text --------
+
+FULL = [("jacobi7.c:jacobi7:0", 256, "f64"), ("d3q19.c:stream_collide:0", 256, "f64"),
+        ("swim.c:calc1:0", 8192, "f64"), ("swim.c:calc2:1", 8192, "f64"), ("swim.c:calc3:2", 8192, "f64"),
+        ("clover.c:ideal_gas:0", 7680, "f64"), ("clover.c:pdv_predict:1", 7680, "f64"),
+        ("clover.c:advec_cell_x:2", 7680, "f64"), ("wave4.c:wave4:0", 512, "f32"),
+        ("zsolve.c:z_solve_lhs:0", 128, "f64")]
+
+
+@pytest.mark.parametrize("kid,size,dtype", FULL, ids=[f[0].split(":")[1] for f in FULL])
+def test_full_size_accsat_bitexact_vs_compiled_reference(kid, size, dtype):
+    """At the BASELINE grid (wave4 at 512^3 and zsolve at 128^3 to bound host
+    memory), one launch of the tuned accsat kernel equals the reference-emitted
+    accsat text compiled by gcc (FMA-rewritten, OpenMP) bit for bit."""
+    torch = _torch()
+    spec = nests.kernel(kid)
+    w = nests.workload(kid, size, dtype=dtype)
+    k = backend.Kernel.lookup(kid)
+    dev = nests.device_inputs(w, native=True, kernel=k)
+    host = {}
+    for n, t in dev.items():
+        host[n] = to_host(t)
+    k.tune(dev, dict(w.scalars), "accsat", reps=1)
+    dev = nests.device_inputs(w, native=True, kernel=k)       # fresh inputs after tuning
+    k.launch(dev, dict(w.scalars), "accsat", "default")
+    got = {n: to_host(t) for n, t in dev.items()}
+    del dev
+    torch.cuda.empty_cache()
+    want = {n: np.ascontiguousarray(a) for n, a in host.items()}
+    oracle_cpu.run(spec, want, w.scalars, "accsat", fma=True, f32=dtype == "f32", threads=os.cpu_count() or 1)
+    for n in w.write_arrays:
+        if not bitwise_equal(got[n], want[n]):
+            diff = np.flatnonzero(got[n].view(np.uint8).reshape(got[n].size, -1).any(axis=1)
+                                  != want[n].view(np.uint8).reshape(want[n].size, -1).any(axis=1))
+            raise AssertionError(f"{kid} full size: '{n}' differs from the compiled reference "
+                                 f"({diff.size} elements differ by zero-ness)")
