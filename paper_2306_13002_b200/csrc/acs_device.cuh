@@ -210,6 +210,10 @@ __global__ void __launch_bounds__(256, MINB) naive_kernel(const __grid_constant_
     }
     NaiveMem<NS, T, ASIS> m{args, pt};
     NS::template body<FORM>(m, args.s, pt);
+    // sharded launch: this thread's write-through stores to peer memory are
+    // performed system-wide before the kernel retires (the signal kernel that
+    // follows on the stream then releases the step flag)
+    if (args.sh.enabled) __threadfence_system();
 }
 
 }  // namespace acs

@@ -767,6 +767,7 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
             }
         }
     }
+    if (args.sh.enabled) __threadfence_system();   // peer write-through visible before the step flag
 }
 
 // ---- host launcher -----------------------------------------------------------

@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(BX* BY) sliced_kernel(const __grid_constant__ 
     pt[2] = x;
     NaiveMem<NS, T, FORM == ACS_ORIGINAL> m{args, pt};
     march_slice<NS, T, FORM, 0>(m, args, pt, slice, kb, ke);
+    if (args.sh.enabled) __threadfence_system();   // peer write-through visible before the step flag
 }
 
 template <class NS, class T, int FORM, int BX, int BY, int KCH>

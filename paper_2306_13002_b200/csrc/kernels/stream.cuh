@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(BX) stream_kernel(const __grid_constant__ Kern
         stage = stage + 1 == S ? 0 : stage + 1;
     }
     cp_async_wait<0>();
+    if (args.sh.enabled) __threadfence_system();   // peer write-through visible before the step flag
 }
 
 template <class NS, class T, int FORM, int BX, int S>
