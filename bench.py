@@ -246,6 +246,7 @@ def main():
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--e2e-eager", action="store_true", help="enqueue the e2e call eagerly instead of a CUDA graph")
+    ap.add_argument("--e2e-split-d2h", action="store_true", help="two download streams in the e2e pipeline")
     ap.add_argument("--e2e-ramp", action="store_true", help="smaller first/last chunks in the e2e pipeline (measured: no gain)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -443,6 +444,7 @@ def e2e_d3q19(args, w, k, dist):
     del dev_rm
     torch.cuda.synchronize()
     runner = pipeline_exec.HostRunner(k, host, w.spec.range_params, chunks=args.e2e_chunks, ramp=args.e2e_ramp)
+    runner.split_d2h = args.e2e_split_d2h
     sc = dict(w.scalars)
 
     def step():

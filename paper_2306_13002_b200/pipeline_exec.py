@@ -126,6 +126,8 @@ class HostRunner:
         self.rm = {n: torch.empty(tuple(t.shape), dtype=t.dtype, device="cuda") for n, t in host.items()}
         self.nat = {n: backend.empty_native(k, n, tuple(t.shape), t.dtype) for n, t in host.items()}
         self.s_h2d, self.s_cmp, self.s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        self.s_d2h2 = torch.cuda.Stream()      # second download stream (a second copy engine)
+        self.split_d2h = False
         self.launches = 0
         self.shell: Dict[str, List] = {}      # store-only arrays: boxes outside the write core
         self._shell_key = None
@@ -195,7 +197,7 @@ class HostRunner:
         cuts = self._cuts(b, n)
         nch = len(cuts) - 1
         cur = torch.cuda.current_stream()
-        for s in (self.s_h2d, self.s_cmp, self.s_d2h):
+        for s in (self.s_h2d, self.s_cmp, self.s_d2h, self.s_d2h2):
             s.wait_stream(cur)
         # whole (non-sliced) arrays once
         whole = [name for name, r in self.reach.items() if not r.sliced and (r.loaded or r.stored)]
@@ -256,11 +258,18 @@ class HostRunner:
             ev2 = torch.cuda.Event()
             ev2.record(self.s_cmp)
             self.s_d2h.wait_event(ev2)
-            with torch.cuda.stream(self.s_d2h):
-                for name, lo, hi in out:
-                    self.host[name][lo:hi].copy_(self.rm[name][lo:hi], non_blocking=True)
-                    self.launches += 1
+            if self.split_d2h:
+                self.s_d2h2.wait_event(ev2)
+            for name, lo, hi in out:
+                mid = (lo + hi) // 2 if self.split_d2h and hi - lo > 1 else hi
+                with torch.cuda.stream(self.s_d2h):
+                    self.host[name][lo:mid].copy_(self.rm[name][lo:mid], non_blocking=True)
+                if mid < hi:
+                    with torch.cuda.stream(self.s_d2h2):
+                        self.host[name][mid:hi].copy_(self.rm[name][mid:hi], non_blocking=True)
+                self.launches += 1
         cur.wait_stream(self.s_d2h)
+        cur.wait_stream(self.s_d2h2)
 
     def capture(self, scalars: Dict[str, float], variant: str = "accsat", schedule="default"):
         """The whole call (every chunk's H2D, remap, launch, remap, D2H on the
