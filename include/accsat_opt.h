@@ -42,6 +42,20 @@ typedef struct {
  * left untouched and its metrics carry the error). */
 int acs_opt_optimize(const char* source, const char* name, const char* variant, const acs_opt_limits* limits,
                      char** text_out, char** json_out);
+/* Differential verification of the optimized form, the reference's
+ * `satcc verify` (proj/tools/satcc_main.cpp:217-283, diff_test in
+ * proj/src/oracle.cpp:12-81): for every region, `trials` random environments
+ * (trial t seeded t + 1; ints U[1, 8], doubles U[-10, 10], mt19937_64) run
+ * the ORIGINAL and the OPTIMIZED region body under the reference's C
+ * semantics (two-rounding fma, bounds-checked arrays, 50M-tick budget); every
+ * scalar and array element of the original's post-state must agree within
+ * tol_rel * max(|a|, |b|) or 1e-12 (NaN never passes; an error is a failure).
+ * *json_out = {"file", "variant", "regions": [{region, function, n_trials,
+ * max_rel_err, max_abs_err, n_failures, failures: [{seed, location, got,
+ * want}] (first 10), ok}]} (free with acs_opt_free).  Returns 0 when every
+ * region passes, 1 when one fails, 2 on a parse / argument error. */
+int acs_opt_verify(const char* source, const char* name, const char* variant, const acs_opt_limits* limits, int trials,
+                   double tol_rel, char** json_out);
 void acs_opt_free(char* p);
 
 #ifdef __cplusplus

@@ -41,6 +41,7 @@
 #include <map>
 #include <memory>
 #include <optional>
+#include <random>
 #include <set>
 #include <sstream>
 #include <stdexcept>
@@ -1930,6 +1931,363 @@ std::string optimize(const std::string& src, const std::string& name, bool sat, 
     return splices.empty() ? src : out;
 }
 
+
+// ============================================================================
+// Interpreter + differential verification (satcc verify)
+//
+// The reference's executor semantics (proj/src/interp.cpp:24-270): scalars are
+// 64-bit ints or doubles; int op int stays int with truncating / and %, /0 and
+// %0 are evaluation errors; anything else is IEEE double; comparisons yield
+// int 0/1; && || short-circuit; fma(a, b, c) = a + b*c with two roundings; the
+// libm calls of known_call; assignments coerce to the target's type; every
+// array access is bounds-checked; a statement budget of 50M ticks.
+// diff_test (proj/src/oracle.cpp:12-81): per trial t (seed t + 1) a random
+// environment — ints U[1, 8], doubles U[-10, 10] for every symbol and array
+// element (mt19937_64) — runs the ORIGINAL and the OPTIMIZED region body;
+// every scalar and array element of the original's post-state must agree
+// within tol_rel * max(|a|, |b|) or 1e-12; NaN never passes; an error in
+// either run is a failure.
+
+struct EvalErr : std::runtime_error {
+    explicit EvalErr(const std::string& m) : std::runtime_error(m) {}
+};
+
+struct Val {
+    bool is_int = true;
+    long long i = 0;
+    double d = 0.0;
+    double as_d() const { return is_int ? (double)i : d; }
+    static Val I(long long v) { return {true, v, 0.0}; }
+    static Val D(double v) { return {false, 0, v}; }
+};
+
+struct Arr {
+    bool is_int = false;
+    std::vector<long long> dims;
+    std::vector<long long> iv;
+    std::vector<double> dv;
+    size_t size() const {
+        size_t n = 1;
+        for (long long d : dims) n *= (size_t)d;
+        return n;
+    }
+};
+
+struct Env {
+    std::map<std::string, Val> sc;
+    std::map<std::string, Arr> arr;
+};
+
+class Interp {
+  public:
+    explicit Interp(Env& e) : env_(e) {}
+    long long ticks = 0;
+    static constexpr long long kBudget = 50000000;
+
+    Val eval(const Expr& e) {
+        switch (e.k) {
+            case Expr::Int: return Val::I(e.iv);
+            case Expr::Float: return Val::D(e.fv);
+            case Expr::Var: {
+                auto it = env_.sc.find(e.text);
+                if (it == env_.sc.end()) throw EvalErr("read of undefined variable: " + e.text);
+                return it->second;
+            }
+            case Expr::Ref: {
+                Arr& a = array(e.text);
+                size_t at = flat(a, e);
+                return a.is_int ? Val::I(a.iv[at]) : Val::D(a.dv[at]);
+            }
+            case Expr::Un: {
+                Val v = eval(*e.kids[0]);
+                if (e.op == "!") return Val::I(v.as_d() == 0.0 ? 1 : 0);
+                return v.is_int ? Val::I(-v.i) : Val::D(-v.d);
+            }
+            case Expr::Bin: return bin(e);
+            case Expr::Call: return call(e);
+        }
+        throw EvalErr("bad expression");
+    }
+
+    void exec(const Stmt& s) {
+        if (++ticks > kBudget) throw EvalErr("evaluation budget exceeded");
+        switch (s.k) {
+            case Stmt::Empty: return;
+            case Stmt::Block:
+                for (auto& c : s.stmts) exec(*c);
+                return;
+            case Stmt::Decl:
+                for (auto& d : s.decls) {
+                    if (!d.dims.empty()) {
+                        Arr a;
+                        a.is_int = s.ty == "int";
+                        a.dims = d.dims;
+                        if (a.is_int) a.iv.assign(a.size(), 0);
+                        else a.dv.assign(a.size(), 0.0);
+                        env_.arr[d.name] = std::move(a);
+                    } else {
+                        Val v = d.init ? eval(*d.init) : (s.ty == "int" ? Val::I(0) : Val::D(0.0));
+                        env_.sc[d.name] = coerce(v, s.ty == "int");
+                    }
+                }
+                return;
+            case Stmt::Assign: assign(*s.lhs, eval(*s.rhs)); return;
+            case Stmt::If:
+                if (eval(*s.cond).as_d() != 0.0) exec(*s.then_s);
+                else if (s.else_s) exec(*s.else_s);
+                return;
+            case Stmt::For:
+                if (s.init) exec(*s.init);
+                while (!s.cond || eval(*s.cond).as_d() != 0.0) {
+                    if (++ticks > kBudget) throw EvalErr("evaluation budget exceeded");
+                    exec(*s.body);
+                    if (s.step) exec(*s.step);
+                }
+                return;
+            case Stmt::Call: (void)eval(*s.call); return;
+        }
+    }
+
+  private:
+    Env& env_;
+
+    Arr& array(const std::string& n) {
+        auto it = env_.arr.find(n);
+        if (it == env_.arr.end()) throw EvalErr("read of undefined array: " + n);
+        return it->second;
+    }
+    size_t flat(const Arr& a, const Expr& r) {
+        if (r.kids.size() != a.dims.size()) throw EvalErr("rank mismatch on " + r.text);
+        size_t at = 0;
+        for (size_t p = 0; p < a.dims.size(); ++p) {
+            Val v = eval(*r.kids[p]);
+            if (!v.is_int) throw EvalErr("non-integer subscript of " + r.text);
+            if (v.i < 0 || v.i >= a.dims[p]) throw EvalErr("index out of bounds on " + r.text);
+            at = at * (size_t)a.dims[p] + (size_t)v.i;
+        }
+        return at;
+    }
+    static Val coerce(Val v, bool to_int) {
+        if (to_int) return v.is_int ? v : Val::I((long long)v.d);
+        return v.is_int ? Val::D((double)v.i) : v;
+    }
+    void assign(const Expr& lhs, Val v) {
+        if (lhs.k == Expr::Var) {
+            auto it = env_.sc.find(lhs.text);
+            if (it == env_.sc.end()) env_.sc[lhs.text] = v;   // first write creates a temp
+            else it->second = coerce(v, it->second.is_int);
+            return;
+        }
+        if (lhs.k == Expr::Ref) {
+            Arr& a = array(lhs.text);
+            size_t at = flat(a, lhs);
+            if (a.is_int) a.iv[at] = coerce(v, true).i;
+            else a.dv[at] = coerce(v, false).d;
+            return;
+        }
+        throw EvalErr("bad assignment target");
+    }
+    Val bin(const Expr& e) {
+        const std::string& op = e.op;
+        if (op == "&&") {
+            if (eval(*e.kids[0]).as_d() == 0.0) return Val::I(0);
+            return Val::I(eval(*e.kids[1]).as_d() != 0.0 ? 1 : 0);
+        }
+        if (op == "||") {
+            if (eval(*e.kids[0]).as_d() != 0.0) return Val::I(1);
+            return Val::I(eval(*e.kids[1]).as_d() != 0.0 ? 1 : 0);
+        }
+        Val a = eval(*e.kids[0]), b = eval(*e.kids[1]);
+        if (a.is_int && b.is_int) {
+            long long x = a.i, y = b.i;
+            if (op == "+") return Val::I(x + y);
+            if (op == "-") return Val::I(x - y);
+            if (op == "*") return Val::I(x * y);
+            if (op == "/") {
+                if (y == 0) throw EvalErr("integer division by zero");
+                return Val::I(x / y);
+            }
+            if (op == "%") {
+                if (y == 0) throw EvalErr("integer modulo by zero");
+                return Val::I(x % y);
+            }
+        } else if (op == "%") {
+            throw EvalErr("'%' on a non-integer operand");
+        }
+        double x = a.as_d(), y = b.as_d();
+        if (op == "<") return Val::I(x < y);
+        if (op == "<=") return Val::I(x <= y);
+        if (op == ">") return Val::I(x > y);
+        if (op == ">=") return Val::I(x >= y);
+        if (op == "==") return Val::I(x == y);
+        if (op == "!=") return Val::I(x != y);
+        volatile double r;   // one IEEE rounding per operation, no contraction
+        if (op == "+") r = x + y;
+        else if (op == "-") r = x - y;
+        else if (op == "*") r = x * y;
+        else if (op == "/") r = x / y;
+        else throw EvalErr("unknown operator " + op);
+        return Val::D(r);
+    }
+    Val call(const Expr& e) {
+        std::vector<double> a;
+        for (auto& k : e.kids) a.push_back(eval(*k).as_d());
+        const std::string& n = e.text;
+        auto need = [&](size_t c) {
+            if (a.size() != c) throw EvalErr("wrong argument count for " + n);
+        };
+        if (n == "fma") {
+            need(3);
+            volatile double p = a[1] * a[2];
+            volatile double r = a[0] + p;   // the interpreter's two-rounding fma
+            return Val::D(r);
+        }
+        if (n == "sqrt") { need(1); return Val::D(std::sqrt(a[0])); }
+        if (n == "fabs") { need(1); return Val::D(std::fabs(a[0])); }
+        if (n == "sin") { need(1); return Val::D(std::sin(a[0])); }
+        if (n == "cos") { need(1); return Val::D(std::cos(a[0])); }
+        if (n == "exp") { need(1); return Val::D(std::exp(a[0])); }
+        if (n == "log") { need(1); return Val::D(std::log(a[0])); }
+        if (n == "floor") { need(1); return Val::D(std::floor(a[0])); }
+        if (n == "ceil") { need(1); return Val::D(std::ceil(a[0])); }
+        if (n == "pow") { need(2); return Val::D(std::pow(a[0], a[1])); }
+        if (n == "fmin") { need(2); return Val::D(std::fmin(a[0], a[1])); }
+        if (n == "fmax") { need(2); return Val::D(std::fmax(a[0], a[1])); }
+        throw EvalErr("call to unknown function: " + n);
+    }
+};
+
+static void region_symbols(const Module& m, const Region& r,
+                           std::vector<std::pair<std::string, std::pair<bool, std::vector<long long>>>>& out) {
+    std::set<std::string> seen;
+    auto add = [&](const std::string& n, bool is_int, const std::vector<long long>& dims) {
+        if (seen.insert(n).second) out.push_back({n, {is_int, dims}});
+    };
+    for (auto& gl : m.globals)
+        for (auto& d : gl->decls) add(d.name, gl->ty == "int", d.dims);
+    for (auto& p : r.fn->params) add(p.name, p.ty == "int", p.dims);
+    std::map<std::string, Sym> locals;
+    collect_decls(*r.fn->body, locals);
+    for (auto& [n, sym] : locals) add(n, sym.is_int, sym.dims);
+    for (auto& v : r.loopvars) add(v, true, {});
+}
+
+static Env random_env(const std::vector<std::pair<std::string, std::pair<bool, std::vector<long long>>>>& syms,
+                      unsigned long long seed) {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> ud(-10.0, 10.0);
+    std::uniform_int_distribution<long long> ui(1, 8);
+    Env e;
+    for (auto& [n, t] : syms) {
+        const bool is_int = t.first;
+        if (t.second.empty()) {
+            e.sc[n] = is_int ? Val::I(ui(rng)) : Val::D(ud(rng));
+        } else {
+            Arr a;
+            a.is_int = is_int;
+            a.dims = t.second;
+            const size_t sz = a.size();
+            if (is_int) {
+                a.iv.resize(sz);
+                for (auto& v : a.iv) v = ui(rng);
+            } else {
+                a.dv.resize(sz);
+                for (auto& v : a.dv) v = ud(rng);
+            }
+            e.arr[n] = std::move(a);
+        }
+    }
+    return e;
+}
+
+struct Failure {
+    unsigned long long seed;
+    std::string location;
+    double got, want;
+};
+
+std::string verify(const std::string& src, const std::string& name, bool sat, bool bulk, const acs_opt_limits& lim,
+                   int trials, double tol_rel, bool& all_ok) {
+    std::string mjson;
+    const std::string opt = optimize(src, name, sat, bulk, lim, mjson);
+    Module m0 = Parser(lex(src)).module();
+    Module m1 = Parser(lex(opt)).module();
+    std::vector<Region> r0, r1;
+    for (auto& f : m0.funcs) {
+        std::vector<std::string> lv;
+        find_in(f, *f.body, lv, r0);
+    }
+    for (auto& f : m1.funcs) {
+        std::vector<std::string> lv;
+        find_in(f, *f.body, lv, r1);
+    }
+    if (r0.size() != r1.size()) throw std::logic_error("optimized output lost a region");
+    all_ok = true;
+    std::ostringstream j;
+    j << "{\"file\": " << json_str(name) << ", \"variant\": "
+      << json_str(sat && bulk ? "accsat" : sat ? "cse+sat" : bulk ? "cse+bulk" : "cse") << ", \"regions\": [";
+    for (size_t k = 0; k < r0.size(); ++k) {
+        std::vector<std::pair<std::string, std::pair<bool, std::vector<long long>>>> syms;
+        region_symbols(m0, r0[k], syms);
+        double max_rel = 0.0, max_abs = 0.0;
+        std::vector<Failure> fails;
+        long long n_fail = 0;
+        for (int t = 0; t < trials; ++t) {
+            const unsigned long long seed = (unsigned long long)t + 1;
+            Env base = random_env(syms, seed);
+            Env want = base, got = base;
+            std::string err;
+            try {
+                Interp(want).exec(*r0[k].anchor->body);
+                Interp(got).exec(*r1[k].anchor->body);
+            } catch (const std::exception& e) {
+                err = e.what();
+            }
+            if (!err.empty()) {
+                ++n_fail;
+                if (fails.size() < 10) fails.push_back({seed, "error: " + err, 0.0, 0.0});
+                continue;
+            }
+            auto cmp = [&](const std::string& loc, double w, double g) {
+                const double ae = std::fabs(g - w), mag = std::max(std::fabs(g), std::fabs(w));
+                const double re = mag > 0.0 ? ae / mag : 0.0;
+                if (ae == ae) max_abs = std::max(max_abs, ae);
+                if (re == re) max_rel = std::max(max_rel, re);
+                if (!(ae <= tol_rel * mag || ae <= 1e-12)) {
+                    ++n_fail;
+                    if (fails.size() < 10) fails.push_back({seed, loc, g, w});
+                }
+            };
+            for (auto& [n, v] : want.sc) {
+                auto it = got.sc.find(n);
+                if (it == got.sc.end()) {
+                    ++n_fail;
+                    if (fails.size() < 10) fails.push_back({seed, n + " (missing)", 0.0, v.as_d()});
+                } else {
+                    cmp(n, v.as_d(), it->second.as_d());
+                }
+            }
+            for (auto& [n, a] : want.arr) {
+                const Arr& b = got.arr[n];
+                for (size_t i = 0; i < a.size(); ++i)
+                    cmp(n + "[" + std::to_string(i) + "]", a.is_int ? (double)a.iv[i] : a.dv[i],
+                        b.is_int ? (double)b.iv[i] : b.dv[i]);
+            }
+        }
+        const bool ok = n_fail == 0;
+        all_ok = all_ok && ok;
+        j << (k ? ", " : "") << "{\"region\": " << k << ", \"function\": " << json_str(r0[k].fn->name)
+          << ", \"n_trials\": " << trials << ", \"max_rel_err\": " << max_rel << ", \"max_abs_err\": " << max_abs
+          << ", \"n_failures\": " << n_fail << ", \"failures\": [";
+        for (size_t f = 0; f < fails.size(); ++f)
+            j << (f ? ", " : "") << "{\"seed\": " << fails[f].seed << ", \"location\": " << json_str(fails[f].location)
+              << ", \"got\": " << fails[f].got << ", \"want\": " << fails[f].want << "}";
+        j << "], \"ok\": " << (ok ? "true" : "false") << "}";
+    }
+    j << "]}";
+    return j.str();
+}
+
 }  // namespace acsopt
 
 extern "C" {
@@ -1958,6 +2316,30 @@ int acs_opt_optimize(const char* source, const char* name, const char* variant, 
         *text_out = dup("");
         *json_out = dup(std::string("{\"error\": ") + acsopt::json_str(e.what()) + "}");
         return 1;
+    }
+}
+
+int acs_opt_verify(const char* source, const char* name, const char* variant, const acs_opt_limits* limits, int trials,
+                   double tol_rel, char** json_out) {
+    acs_opt_limits lim{10000, 10.0, 10, 1};
+    if (limits) lim = *limits;
+    std::string v = variant ? variant : "accsat";
+    auto dup = [](const std::string& s) {
+        char* p = static_cast<char*>(std::malloc(s.size() + 1));
+        std::memcpy(p, s.c_str(), s.size() + 1);
+        return p;
+    };
+    try {
+        if (v != "accsat" && v != "cse+sat" && v != "cse+bulk" && v != "cse")
+            throw std::invalid_argument("unknown variant: " + v + " (expected cse, cse+sat, cse+bulk, or accsat)");
+        bool ok = true;
+        std::string json = acsopt::verify(source ? source : "", name ? name : "<input>", v == "accsat" || v == "cse+sat",
+                                          v == "accsat" || v == "cse+bulk", lim, trials, tol_rel, ok);
+        *json_out = dup(json);
+        return ok ? 0 : 1;
+    } catch (const std::exception& e) {
+        *json_out = dup(std::string("{\"error\": ") + acsopt::json_str(e.what()) + "}");
+        return 2;
     }
 }
 

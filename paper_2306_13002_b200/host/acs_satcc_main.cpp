@@ -3,6 +3,10 @@
 //
 //   acs-satcc [opt] [--variant V] [-o FILE] file        optimized source
 //   acs-satcc report [--variant V] file...              satcc-metrics-v1 JSON
+//   acs-satcc verify [--variant V] [--trials N] [--tol T] file...
+//                                                       satcc-verify-v1 JSON: differential
+//        run of original vs optimized region bodies under the reference's
+//        interpreter semantics (diff_test, proj/src/oracle.cpp:12-81)
 //   acs-satcc [--variant V] [--keep] -- cmd args...     wrapper mode: every
 //        existing *.c argument is optimized into <tmp>/<argidx>/<basename> and
 //        cmd runs on the substituted paths; exit code propagated (128+signal,
@@ -41,7 +45,9 @@ int main(int argc, char** argv) {
     bool no_sat = false, no_bulk = false, keep = false;
     std::vector<std::string> files, child;
     size_t i = 0;
-    if (!args.empty() && (args[0] == "opt" || args[0] == "report")) cmd = args[i++];
+    if (!args.empty() && (args[0] == "opt" || args[0] == "report" || args[0] == "verify")) cmd = args[i++];
+    int trials = 20;
+    double tol_rel = 1e-6;   // satcc's default --tol (proj/tools/satcc_main.cpp:51)
     for (; i < args.size(); ++i) {
         const std::string& a = args[i];
         auto next = [&]() -> std::string {
@@ -64,6 +70,8 @@ int main(int argc, char** argv) {
         else if (a == "--no-sat") no_sat = true;
         else if (a == "--no-bulk") no_bulk = true;
         else if (a == "--keep") keep = true;
+        else if (a == "--trials") trials = std::stoi(next());
+        else if (a == "--tol") tol_rel = std::stod(next());
         else files.push_back(a);
     }
     bool sat = variant == "accsat" || variant == "cse+sat", bulk = variant == "accsat" || variant == "cse+bulk";
@@ -138,8 +146,41 @@ int main(int argc, char** argv) {
     }
 
     if (files.empty()) {
-        std::cerr << "usage: acs-satcc [opt|report] [--variant V] file...  |  acs-satcc [flags] -- cmd args...\n";
+        std::cerr << "usage: acs-satcc [opt|report|verify] [--variant V] file...  |  acs-satcc [flags] -- cmd args...\n";
         return 2;
+    }
+    if (cmd == "verify") {   // satcc-verify-v1 (proj/tools/satcc_main.cpp:217-283)
+        int rc = 0;
+        bool all_ok = true;
+        std::string out = "{\"schema\": \"satcc-verify-v1\", \"trials\": " + std::to_string(trials) +
+                          ", \"tol_rel\": " + std::to_string(tol_rel) + ", \"files\": [";
+        bool first = true;
+        for (const std::string& f : files) {
+            char* j = nullptr;
+            std::string src;
+            try {
+                src = read_file(f);
+            } catch (const std::exception& e) {
+                std::cerr << "acs-satcc: error: " << e.what() << "\n";
+                rc = 1;
+                continue;
+            }
+            int r = acs_opt_verify(src.c_str(), f.c_str(), v.c_str(), &lim, trials, tol_rel, &j);
+            std::string js = j;
+            acs_opt_free(j);
+            if (r == 2) {
+                std::cerr << "acs-satcc: error: " << f << ": " << js << "\n";
+                rc = 1;
+                continue;
+            }
+            if (r == 1) all_ok = false;
+            out += (first ? "" : ", ") + js;
+            first = false;
+        }
+        out += std::string("], \"ok\": ") + (all_ok ? "true" : "false") + "}";
+        std::cout << out << "\n";
+        if (!all_ok) rc = 1;
+        return rc;
     }
     int rc = 0;
     std::string reports = "[";

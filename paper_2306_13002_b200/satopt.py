@@ -33,6 +33,9 @@ def lib():
         L.acs_opt_optimize.restype = ctypes.c_int
         L.acs_opt_optimize.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(Limits),
                                        ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]
+        L.acs_opt_verify.restype = ctypes.c_int
+        L.acs_opt_verify.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(Limits),
+                                     ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_void_p)]
         L.acs_opt_free.argtypes = [ctypes.c_void_p]
         _lib = L
     return _lib
@@ -51,3 +54,19 @@ def optimize_source(source: str, name: str = "<input>", variant: str = "accsat",
     if rc != 0:
         raise SyntaxError(meta.get("error", "parse failure"))
     return text, meta
+
+
+def verify_source(source: str, name: str = "<input>", variant: str = "accsat", trials: int = 20,
+                  tol_rel: float = 1e-6, max_nodes: int = 10000, max_time_s: float = 10.0, max_iters: int = 10,
+                  dag_search: bool = True) -> Tuple[bool, dict]:
+    """satcc verify for one source: (all regions ok, per-file report)."""
+    lim = Limits(max_nodes, max_time_s, max_iters, 1 if dag_search else 0)
+    j = ctypes.c_void_p()
+    rc = lib().acs_opt_verify(source.encode(), name.encode(), variant.encode(), ctypes.byref(lim), trials, tol_rel,
+                              ctypes.byref(j))
+    rep = json.loads(ctypes.string_at(j).decode())
+    lib().acs_opt_free(j)
+    if rc == 2:
+        raise SyntaxError(rep.get("error", "parse failure"))
+    return rc == 0, rep
+

@@ -151,3 +151,50 @@ def test_own_stage_a_output_lowers_to_device_bodies(nest):
         low = lowering.lower_text(text, r["function"], fma=True)
         assert low.n_fma == r["fma_count"]
         assert low.n_loads == r["static_loads_after"]
+
+
+# ---- verify (satcc verify: differential run under the reference's semantics) ----
+
+def shrunk(nest, dim):
+    """A nest text with its declared array extents cut to `dim` (random loop
+    bounds are U[1, 8], as in the reference's random_env)."""
+    src = open(os.path.join(ROOT, "nests", f"{nest}.c")).read()
+    for big in ("1028", "8193", "7684", "258"):
+        src = src.replace(f"[{big}]", f"[{dim}]")
+    return src
+
+
+@pytest.mark.parametrize("nest", ["jacobi7", "d3q19", "swim", "zsolve"])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_verify_own_output_passes(nest, variant):
+    ok, rep = satopt.verify_source(shrunk(nest, 12), f"{nest}.c", variant, trials=8)
+    assert ok, json.dumps(rep)[:2000]
+    assert all(r["n_trials"] == 8 and r["ok"] for r in rep["regions"])
+
+
+def test_verify_counts_errors_as_failures():
+    """An evaluation error (int division by zero) in a trial is a failure,
+    as in diff_test (proj/src/oracle.cpp:73-78)."""
+    src = """double A[8];
+void f(void) {
+    int i;
+    #pragma acc parallel loop gang
+    for (i = 1; i < 7; i++) {
+        A[i] = A[i] + 1 / (i - i);
+    }
+}
+"""
+    ok, rep = satopt.verify_source(src, "bad.c", "accsat", trials=3)
+    assert not ok
+    r = rep["regions"][0]
+    assert r["n_failures"] == 3 and "division by zero" in r["failures"][0]["location"]
+
+
+def test_cli_verify_schema(tmp_path):
+    k = tmp_path / "k.c"
+    k.write_text(shrunk("jacobi7", 10))
+    r = subprocess.run([satopt.CLI_PATH, "verify", "--trials", "4", str(k)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    doc = json.loads(r.stdout)
+    assert doc["schema"] == "satcc-verify-v1" and doc["ok"] and doc["trials"] == 4
+    assert doc["files"][0]["regions"][0]["function"] == "jacobi7"

@@ -94,3 +94,11 @@ def test_corpus_kernel(path, variant):
                 if name.startswith("_"):
                     continue
                 assert close(got[0][name][1], v), f"{os.path.basename(path)}:{fn}/{variant}: scalar {name}"
+
+
+@pytest.mark.parametrize("path", CORPUS, ids=[os.path.basename(p) for p in CORPUS])
+def test_corpus_verify(path):
+    """acs-satcc verify on every reference corpus kernel (accsat, 10 trials)."""
+    ok, rep = satopt.verify_source(open(path).read(), os.path.basename(path), "accsat", trials=10)
+    bad = [r for r in rep["regions"] if not r["ok"]]
+    assert ok, json.dumps(bad)[:2000]
