@@ -1,3 +1,5 @@
+# ncu --set full of every nest's tuned accsat kernel, summarised on the box (reports are large).
+# usage: gpurun -- bash tools/gpu/profile_all.sh
 # ncu --set full of every nest's tuned accsat kernel (one launch each)
 mkdir -p gpurun_out
 cap() {  # name kid slot [f32]

@@ -1,3 +1,5 @@
+# Round-end check on one GPU: GPU tests, smoke, bench (both arms), ncu launch list.
+# usage: gpurun -- bash tools/gpu/round_check.sh
 # full round check: gpu tests, smoke, bench (both arms), launch list
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1

@@ -1,3 +1,4 @@
+# GPU tests + the N=2 bench path with both ranks on one GPU (functional check only).
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 tail -3 gpurun_out/pytest_gpu.log
