@@ -250,6 +250,8 @@ def main():
     ap.add_argument("--e2e-ramp", action="store_true", help="smaller first/last chunks in the e2e pipeline (measured: no gain)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if isinstance(args.schedule, str) and args.schedule.isdigit():
+        args.schedule = int(args.schedule)     # an explicit registered slot (0 = naive)
 
     if args.impl == "reference":
         return reference_arm(args)
@@ -306,7 +308,9 @@ def main():
                        "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                        "traffic": load_traffic("stream_collide"),
                        "kernel": f"stream_collide {args.variant}: " + (
-                           k.info["schedules"][0][tuned_slot] if tuned_slot is not None else args.schedule)}
+                           k.info["schedules"][0][tuned_slot] if tuned_slot is not None
+                           else (k.info["schedules"][0][args.schedule] if isinstance(args.schedule, int)
+                                 else args.schedule))}
     out["config"]["tuned"] = {"slot": tuned_slot, "ms_per_slot": {str(s): round(v, 4) for s, v in tuned_ms.items()}}
     out["clocks"] = clk.summary()
 

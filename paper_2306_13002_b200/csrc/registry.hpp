@@ -5,6 +5,7 @@
 #pragma once
 
 #include <array>
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 
@@ -194,7 +195,14 @@ acs_status launch_naive(const LaunchReq& r) {
         block = dim3(256, 1, 1);
         grid = dim3((unsigned)((nx + 255) / 256), 1, 1);
     } else {
-        const unsigned bx = nx >= 128 ? 128 : 32;
+        // a CTA covers whole rows of the innermost loop when they fit (256):
+        // row-shifted stores (D3Q19 pushes) then share a 32-byte sector only
+        // with stores of the same CTA (fewer partial-sector read-modify-writes)
+        static const unsigned bx_env = [] {
+            const char* e = std::getenv("ACS_NAIVE_BX");
+            return e ? (unsigned)std::atoi(e) : 0u;
+        }();
+        const unsigned bx = bx_env && nx >= (long long)bx_env ? bx_env : (nx >= 256 ? 256 : nx >= 128 ? 128 : 32);
         const unsigned by = 256 / bx;
         const long long ny = ka.hi[NL - 2] - ka.lo[NL - 2];
         block = dim3(bx, by, 1);
