@@ -214,9 +214,13 @@ __global__ void __launch_bounds__(BX* BY) sliced_kernel(const __grid_constant__ 
     constexpr int NSL = NS::nslices[FORM];
     const int slice = (int)(blockIdx.z % NSL);
     const int chunk = (int)(blockIdx.z / NSL);
-    const int x = args.lo[2] + (int)(blockIdx.x * BX + threadIdx.x);
+    // x tiles start at a 128-byte-aligned column (x0 = lo aligned down), so a
+    // 32-byte sector of a stored row is written by one CTA only
+    const int xlo = (int)args.lo[2];
+    const int x0 = xlo - (((xlo % 16) + 16) % 16);
+    const int x = x0 + (int)(blockIdx.x * BX + threadIdx.x);
     const int y = args.lo[1] + (int)(blockIdx.y * BY + threadIdx.y);
-    if (x >= args.hi[2] || y >= args.hi[1]) return;
+    if (x < xlo || x >= args.hi[2] || y >= args.hi[1]) return;
     const int kb = args.lo[0] + chunk * kchunk;
     const int ke = min(kb + kchunk, (int)args.hi[0]);
     int pt[3];
@@ -234,7 +238,8 @@ acs_status launch_sliced(const LaunchReq& r) {
     acs_status st = bind<NS, std::is_same<T, float>::value>(r, ka, empty);
     if (st != ACS_OK || empty) return st;
     constexpr int NSL = NS::nslices[FORM];
-    const long long nx = ka.hi[2] - ka.lo[2], ny = ka.hi[1] - ka.lo[1], nz = ka.hi[0] - ka.lo[0];
+    const long long x0 = ka.lo[2] - (((ka.lo[2] % 16) + 16) % 16);
+    const long long nx = ka.hi[2] - x0, ny = ka.hi[1] - ka.lo[1], nz = ka.hi[0] - ka.lo[0];
     const long long chunks = (nz + KCH - 1) / KCH;
     dim3 grid((unsigned)((nx + BX - 1) / BX), (unsigned)((ny + BY - 1) / BY), (unsigned)(chunks * NSL));
     sliced_kernel<NS, T, FORM, BX, BY><<<grid, dim3(BX, BY, 1), 0, r.stream>>>(ka, KCH);
