@@ -216,4 +216,36 @@ __global__ void __launch_bounds__(256, MINB) naive_kernel(const __grid_constant_
     if (args.sh.enabled) __threadfence_system();
 }
 
+// R points per thread along the innermost loop, strided by the block width
+// (each r-slice of a warp is still one coalesced row segment): R
+// independent bodies per thread, so the read-only (ld.global.nc) loads of
+// all R points can be in flight together — more bytes in flight per SM for
+// point-local streaming nests (ideal_gas, calc3) at the same occupancy.
+template <class NS, class T, int FORM, int R>
+__global__ void __launch_bounds__(256) naive_multi_kernel(const __grid_constant__ KernelArgs<NS> args) {
+    constexpr int NL = NS::NLOOP;
+    int pt[NL];
+    if constexpr (NL >= 2) {
+        const int y = args.lo[NL - 2] + (int)(blockIdx.y * blockDim.y + threadIdx.y);
+        if (y >= args.hi[NL - 2]) return;
+        pt[NL - 2] = y;
+    }
+    if constexpr (NL >= 3) {
+        const int z = args.lo[NL - 3] + (int)blockIdx.z;
+        if (z >= args.hi[NL - 3]) return;
+        pt[NL - 3] = z;
+    }
+    const int x0 = args.lo[NL - 1] + (int)(blockIdx.x * blockDim.x * R + threadIdx.x);
+    NaiveMem<NS, T, FORM == 0> m{args, pt};
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int x = x0 + r * (int)blockDim.x;
+        if (x < args.hi[NL - 1]) {
+            pt[NL - 1] = x;
+            NS::template body<FORM>(m, args.s, pt);
+        }
+    }
+    if (args.sh.enabled) __threadfence_system();
+}
+
 }  // namespace acs

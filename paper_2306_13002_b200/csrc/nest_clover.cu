@@ -13,6 +13,8 @@ void register_clover() {
         e.function = "ideal_gas";
         describe<gen::ideal_gas>(e, "clover.c", 0);
         fill_naive<gen::ideal_gas, double>(e, 0);
+        fill_naive_multi<gen::ideal_gas, double, 2>(e, 0);
+        fill_naive_multi<gen::ideal_gas, double, 4>(e, 0);
         fill_stream<gen::ideal_gas, double, 128, 3>(e, 0);
         fill_stream<gen::ideal_gas, double, 256, 4>(e, 0);
         fill_march<gen::ideal_gas, double, 0, 128, 1, 128, 1, 3>(e, 0);

@@ -13,6 +13,8 @@ void register_swim() {
         e.function = "calc1";
         describe<gen::calc1>(e, "swim.c", 0);
         fill_naive<gen::calc1, double>(e, 0);
+        fill_naive_multi<gen::calc1, double, 2>(e, 0);
+        fill_naive_multi<gen::calc1, double, 4>(e, 0);
         fill_march<gen::calc1, double, 0, 128, 1, 128, 1, 3>(e, 0);
         fill_march<gen::calc1, double, 0, 128, 1, 64, 1, 3>(e, 0);
         fill_march<gen::calc1, double, 0, 64, 1, 64, 1, 4>(e, 0);
@@ -36,6 +38,8 @@ void register_swim() {
         e.function = "calc3";
         describe<gen::calc3>(e, "swim.c", 2);
         fill_naive<gen::calc3, double>(e, 0);
+        fill_naive_multi<gen::calc3, double, 2>(e, 0);
+        fill_naive_multi<gen::calc3, double, 4>(e, 0);
         fill_stream<gen::calc3, double, 128, 3>(e, 0);
         fill_stream<gen::calc3, double, 256, 4>(e, 0);
         fill_march<gen::calc3, double, 0, 128, 1, 128, 1, 3>(e, 0);

@@ -215,6 +215,40 @@ acs_status launch_naive(const LaunchReq& r) {
     return check_launch(NS::array_names[0]);
 }
 
+template <class NS, class T, int FORM, int R>
+acs_status launch_naive_multi(const LaunchReq& r) {
+    KernelArgs<NS> ka;
+    bool empty = false;
+    acs_status st = bind<NS, std::is_same<T, float>::value>(r, ka, empty);
+    if (st != ACS_OK || empty) return st;
+    constexpr int NL = NS::NLOOP;
+    static_assert(NL >= 2, "naive_multi: 2-D / 3-D nests");
+    const long long nx = ka.hi[NL - 1] - ka.lo[NL - 1];
+    const unsigned bx = nx >= 128 * R ? 128 : 32;
+    const unsigned by = 256 / bx;
+    const long long ny = ka.hi[NL - 2] - ka.lo[NL - 2];
+    dim3 block(bx, by, 1);
+    dim3 grid((unsigned)((nx + (long long)bx * R - 1) / ((long long)bx * R)), (unsigned)((ny + by - 1) / by),
+              NL >= 3 ? (unsigned)(ka.hi[0] - ka.lo[0]) : 1u);
+    naive_multi_kernel<NS, T, FORM, R><<<grid, block, 0, r.stream>>>(ka);
+    return check_launch(NS::array_names[0]);
+}
+
+// naive with R points per thread (ORIGINAL registered too for parity coverage:
+// its as-written loads are ordered, so its R bodies do not overlap)
+template <class NS, class T, int R>
+void fill_naive_multi(Entry& e, int prec) {
+    const int slot = e.n_sched[prec]++;
+    e.launch[prec][0][slot] = &launch_naive_multi<NS, T, 0, R>;
+    e.launch[prec][1][slot] = &launch_naive_multi<NS, T, 1, R>;
+    e.launch[prec][2][slot] = &launch_naive_multi<NS, T, 2, R>;
+    e.launch[prec][3][slot] = &launch_naive_multi<NS, T, 3, R>;
+    e.launch[prec][4][slot] = &launch_naive_multi<NS, T, 4, R>;
+    e.sched_name[prec][slot] = "naive, " + std::to_string(R) + " points per thread";
+    for (int v = 1; v < 5; ++v)
+        if (e.best[prec][v] == 0) e.best[prec][v] = slot;
+}
+
 template <class NS, class T>
 void fill_naive(Entry& e, int prec) {
     e.launch[prec][0][0] = &launch_naive<NS, T, 0>;
