@@ -142,6 +142,7 @@ class _Lowerer:
         self.static_refs: set = set()
         self.static_stores: set = set()
         self.cur_refs: Optional[set] = None
+        self.dead: set = set()          # ids of assignments under never-true guards
         self.slice_refs: List[list] = []
 
     # -- types
@@ -172,9 +173,108 @@ class _Lowerer:
     def count_assigns(self, s: ks.Stmt):
         if s.kind == "assign" and s.lhs.kind == "var":
             self.assign_count[s.lhs.op] = self.assign_count.get(s.lhs.op, 0) + 1
-            self.int_assigns.setdefault(s.lhs.op, []).append(s.rhs)
+            if id(s) not in self.dead:        # never executed: no candidate value
+                self.int_assigns.setdefault(s.lhs.op, []).append(s.rhs)
         for c in ks.children(s):
             self.count_assigns(c)
+
+    # -- guards the loop bounds decide ---------------------------------------
+    #
+    # advec's `if (upwind > nx - 1) upwind = nx - 1;` follows `upwind = j + 1`
+    # inside `for (j = 2; j < nx - 2; j++)`: j + 1 <= nx - 2 < nx - 1, so the
+    # clamp never runs and upwind's candidate values are {j - 2, j + 1} — all
+    # affine in j, so its loads can be served from the staged box unchecked.
+    # Symbolic linear forms over loop variables and scalar parameters
+    # ({name: coeff}, const); a guard is dead when its comparison is false at
+    # every point of the iteration space.
+
+    def lin(self, e: ks.Expr, env) -> Optional[Tuple[Dict[str, int], int]]:
+        if e.kind == "int":
+            return {}, int(e.text)
+        if e.kind == "var":
+            if e.op in env:
+                return env[e.op]
+            if e.op in self.loop_vars or (self.types.get(e.op) == "int" and e.op in self.fn_param_names):
+                return {e.op: 1}, 0
+            return None
+        if e.kind == "bin" and e.op in ("+", "-"):
+            a, b = self.lin(e.kids[0], env), self.lin(e.kids[1], env)
+            if a is None or b is None:
+                return None
+            sg = 1 if e.op == "+" else -1
+            co = dict(a[0])
+            for k, v in b[0].items():
+                co[k] = co.get(k, 0) + sg * v
+            return {k: v for k, v in co.items() if v}, a[1] + sg * b[1]
+        return None
+
+    def always_false(self, cond: ks.Expr, env) -> bool:
+        """cond (a < b, a <= b, a > b, a >= b) false at every iteration-space point."""
+        if cond.kind != "bin" or cond.op not in ("<", "<=", ">", ">="):
+            return False
+        a, b = self.lin(cond.kids[0], env), self.lin(cond.kids[1], env)
+        if a is None or b is None:
+            return False
+        # d = a - b; the guard holds when d > 0 (>), d >= 0 (>=), d < 0 (<), d <= 0 (<=)
+        co = dict(a[0])
+        for k, v in b[0].items():
+            co[k] = co.get(k, 0) - v
+        const = a[1] - b[1]
+        co = {k: v for k, v in co.items() if v}
+        want_pos = cond.op in (">", ">=")
+        strict = cond.op in (">", "<")
+        # extreme of d over the loop ranges: loop var v in [lo_v, hi_v - 1]
+        ext, ext_c = {}, const
+        for v, c in co.items():
+            if v not in self.loop_ranges:
+                ext[v] = ext.get(v, 0) + c       # parameters stay symbolic
+                continue
+            (lo, lo_c), (hi, hi_c) = self.loop_ranges[v]
+            take_hi = (c > 0) == want_pos        # maximise d for >, minimise for <
+            form, fc = (hi, hi_c - 1) if take_hi else (lo, lo_c)
+            for k, w in form.items():
+                ext[k] = ext.get(k, 0) + c * w
+            ext_c += c * fc
+        if any(w for w in ext.values()):
+            return False                        # still depends on a parameter
+        if want_pos:
+            return ext_c <= 0 if strict else ext_c < 0
+        return ext_c >= 0 if strict else ext_c > 0
+
+    def find_dead(self, s: ks.Stmt, env, out: set):
+        """Walk the body in order, tracking int scalars with linear values;
+        collect the assignments under guards that can never hold."""
+        k = s.kind
+        if k == "block":
+            for c in s.stmts:
+                self.find_dead(c, env, out)
+        elif k == "assign" and s.lhs.kind == "var":
+            v = self.lin(s.rhs, env)
+            if v is not None:
+                env[s.lhs.op] = v
+            else:
+                env.pop(s.lhs.op, None)
+        elif k == "if":
+            if self.always_false(s.cond, env):
+                self.mark_dead(s.then_s, out)
+                if s.else_s is not None:
+                    self.find_dead(s.else_s, env, out)
+                return
+            e1, e2 = dict(env), dict(env)
+            self.find_dead(s.then_s, e1, out)
+            if s.else_s is not None:
+                self.find_dead(s.else_s, e2, out)
+            for name in set(e1) | set(e2) | set(env):   # keep only values both arms agree on
+                if e1.get(name) == e2.get(name) and name in e1:
+                    env[name] = e1[name]
+                else:
+                    env.pop(name, None)
+
+    def mark_dead(self, s: ks.Stmt, out: set):
+        if s.kind == "assign":
+            out.add(id(s))
+        for c in ks.children(s):
+            self.mark_dead(c, out)
 
     def as_affine(self, e: ks.Expr) -> Optional[Affine]:
         if e.kind == "int":
@@ -767,6 +867,17 @@ class _Lowerer:
     def run(self) -> Lowered:
         body_stmt = self.region.anchor.body
         self.body_stmt = body_stmt
+        # loop ranges as linear forms of the parameters (for dead guards)
+        self.fn_param_names = {p.name for p in self.fn.params if not p.dims}
+        self.loop_ranges = {}
+        for l in self.region.loops:
+            lo = self.lin(l.init.rhs, {}) if l.init is not None and l.init.kind == "assign" else None
+            hi = self.lin(l.cond.kids[1], {}) if l.cond is not None and l.cond.kind == "bin" else None
+            if lo is not None and hi is not None and l.cond.op in ("<", "<="):
+                if l.cond.op == "<=":
+                    hi = (hi[0], hi[1] + 1)
+                self.loop_ranges[l.loop_var] = (lo, hi)
+        self.find_dead(body_stmt, {}, self.dead)
         self.count_assigns(body_stmt)
         # function-level locals other than loop vars
         pre: List[str] = []

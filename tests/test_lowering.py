@@ -161,10 +161,34 @@ def test_generated_headers_are_current(tmp_path):
 
 
 def test_value_set_proven_dynamic_loads():
-    """advec: donor / downwind take only affine candidates (j-1 or j) -> ldx_in
-    (no range check); upwind can be the clamp nx-1 (not affine in j) -> ldx."""
+    """advec: donor / downwind take only affine candidates (j-1 or j); the
+    upwind clamp `if (upwind > nx - 1) upwind = nx - 1` after `upwind = j + 1`
+    can never fire inside `for (j = 2; j < nx - 2; j++)`, so upwind's
+    candidates are {j-2, j+1} too -> every dynamic load is ldx_in."""
     low = lower(emitted("clover", "accsat"), "advec_cell_x")
     assert re.search(r"ldx_in<ARR_density1>\(k, donor\)", low.body)
     assert re.search(r"ldx_in<ARR_pre_vol>\(k, donor\)", low.body)
-    assert re.search(r"ldx<ARR_density1>\(k, upwind\)", low.body)
-    assert not re.search(r"ldx_in<ARR_density1>\(k, upwind\)", low.body)
+    assert re.search(r"ldx_in<ARR_density1>\(k, upwind\)", low.body)
+    assert not re.search(r"ldx<", low.body)
+
+
+CLAMP = """void f(double a[64], double b[64], int n) {
+    int i, u;
+    #pragma acc parallel loop gang
+    for (i = 1; i < n - LIMIT; i++) {
+        u = i + 1;
+        if (u > n - 1) {
+            u = n - 1;
+        }
+        b[i] = a[u];
+    }
+}
+"""
+
+
+def test_dead_guard_needs_the_loop_bound():
+    """The clamp is dead only if i + 1 <= n - 1 for every i of the loop."""
+    dead = lower(CLAMP.replace("LIMIT", "2"), "f", fma=False)       # i <= n - 3: dead
+    assert "ldx_in<ARR_a>(u)" in dead.body
+    live = lower(CLAMP.replace("LIMIT", "0"), "f", fma=False)       # i = n - 1 reaches it
+    assert "ldx<ARR_a>(u)" in live.body and "ldx_in" not in live.body
