@@ -16,8 +16,9 @@ void register_jacobi7() {
         fill_march<gen::jacobi7, double, 0, 64, 8, 64, 2, 3>(e, 0);
         fill_march<gen::jacobi7, double, 0, 32, 16, 32, 4, 3>(e, 0);
         fill_march<gen::jacobi7, double, 0, 128, 4, 128, 2, 2>(e, 0);
+        fill_march<gen::jacobi7, double, 0, 128, 8, 128, 2, 2>(e, 0);
+        fill_march<gen::jacobi7, double, 0, 128, 4, 128, 1, 2>(e, 0);
         fill_march<gen::jacobi7, double, 0, 128, 8, 64, 4, 2, 2>(e, 0);
-        fill_march<gen::jacobi7, double, 0, 128, 4, 64, 4, 2, 2>(e, 0);
         register_entry(&e);
     }
 }
