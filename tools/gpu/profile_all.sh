@@ -3,14 +3,14 @@
 # ncu --set full of every nest's tuned accsat kernel (one launch each)
 mkdir -p gpurun_out
 cap() {  # name kid slot [f32]
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:'naive_kernel|march_kernel|stream_kernel|sliced_kernel' -s 1 -c 1 -o gpurun_out/r01_$1 python tools/gpu/profile_kernel.py $2 accsat $3 $4 3 > gpurun_out/ncu_$1.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:'naive_kernel|naive_multi_kernel|march_kernel|stream_kernel|sliced_kernel' -s 1 -c 1 -o gpurun_out/r01_$1 python tools/gpu/profile_kernel.py $2 accsat $3 $4 3 > gpurun_out/ncu_$1.log 2>&1
 }
 cap jacobi7 jacobi7.c:jacobi7:0 20
 cap d3q19 d3q19.c:stream_collide:0 17
 cap calc1 swim.c:calc1:0 17
 cap calc2 swim.c:calc2:1 17
 cap calc3 swim.c:calc3:2 16
-cap ideal_gas clover.c:ideal_gas:0 16
+cap ideal_gas clover.c:ideal_gas:0 18
 cap pdv clover.c:pdv_predict:1 17
 cap advec clover.c:advec_cell_x:2 17
 cap wave4 wave4.c:wave4:0 20 f32
