@@ -235,6 +235,12 @@ acs_status acs_copy(const acs_array* dst, const acs_array* src, void* cuda_strea
 acs_status acs_native_strides(const acs_kernel* k, const char* array_name, int ndim,
                               const int64_t* dims, int64_t* strides_out);
 
+/* Element offset the backend prefers for the start of array `array_name`
+ * (0 for most arrays): q-major SoA component planes are shifted so the first
+ * interior point of every row starts a 32-byte sector.  Allocate
+ * offset + span elements and pass data + offset as acs_array.data. */
+acs_status acs_native_offset(const acs_kernel* k, const char* array_name, int elem_size, int64_t* offset_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -268,12 +268,23 @@ def copy(dst, src, stream=None) -> None:
 
 
 def empty_native(kernel: Kernel, name: str, dims, dtype, device="cuda"):
-    """Device tensor with the backend's preferred strides for `name`."""
+    """Device tensor with the backend's preferred strides and start offset for
+    `name` (acs_native_strides / acs_native_offset)."""
     torch = _torch()
     st = kernel.native_strides(name, tuple(dims))
     n = int(np.prod(dims))
-    return torch.empty_strided(tuple(dims), st, dtype=dtype, device=device) if n else \
-        torch.empty(tuple(dims), dtype=dtype, device=device)
+    if not n:
+        return torch.empty(tuple(dims), dtype=dtype, device=device)
+    esize = torch.empty((), dtype=dtype).element_size()
+    off = ctypes.c_int64()
+    f = lib().acs_native_offset
+    f.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_void_p]
+    _check(f(kernel.handle, name.encode(), esize, ctypes.byref(off)), "acs_native_offset")
+    if off.value == 0:
+        return torch.empty_strided(tuple(dims), st, dtype=dtype, device=device)
+    span = 1 + sum((d - 1) * s for d, s in zip(dims, st))
+    flat = torch.empty(off.value + span, dtype=dtype, device=device)
+    return flat.as_strided(tuple(dims), st, off.value)
 
 
 # ---------------------------------------------------------------------------

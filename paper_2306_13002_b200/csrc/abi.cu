@@ -642,4 +642,27 @@ acs_status acs_native_strides(const acs_kernel* k, const char* array_name, int n
     return ACS_OK;
 }
 
+acs_status acs_native_offset(const acs_kernel* k, const char* array_name, int elem_size, int64_t* offset_out) {
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    if (!e || !array_name || !offset_out || elem_size <= 0) {
+        set_error("acs_native_offset: bad argument");
+        return ACS_E_ARG;
+    }
+    *offset_out = 0;
+    // q-major SoA component planes (D3Q19): shift the array by a few elements so
+    // the first interior point of every row (x = the loop's constant lower
+    // bound) starts a 32-byte sector — interior rows then read and write whole
+    // sectors (no over-fetch of the ghost column, no read-modify-write of a
+    // sector shared with it).  Only for the SoA arrays, whose kernels do not
+    // use the TMA (which needs 16-byte-aligned bases).
+    bool comp = false;
+    for (size_t i = 0; i < e->arrays.size(); ++i)
+        if (e->arrays[i] == array_name) comp = e->component_last[i] != 0;
+    if (e->soa_last_dim && comp && e->inner_lo > 0 && 32 % elem_size == 0) {
+        const int per = 32 / elem_size;
+        *offset_out = (per - e->inner_lo % per) % per;
+    }
+    return ACS_OK;
+}
+
 }  // extern "C"

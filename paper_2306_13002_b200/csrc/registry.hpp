@@ -48,6 +48,7 @@ struct Entry {
     int n_sched[2] = {1, 1};     // slot 0 (naive) always present once registered
     int best[2][6] = {};         // preferred slot per (precision, variant); acs_tune updates it
     bool soa_last_dim = false;   // backend layout: trailing component subscript made slowest (D3Q19 q)
+    int inner_lo = -999;         // the innermost loop's constant lower bound (native row offset)
     std::vector<int> component_last;  // per array: trailing subscript is an absolute component index
     struct Reach {
         int sliced, loaded, stored, ld_lo, ld_hi, st_lo, st_hi;
@@ -294,6 +295,7 @@ acs_status eval_space(const acs_scalar* sc, int n, long long* lo, long long* hi)
 template <class NS>
 void describe(Entry& e, const char* file, int region) {
     e.space = &eval_space<NS>;
+    e.inner_lo = NS::inner_lo_const;
     e.region = region;
     e.n_loops = NS::NLOOP;
     for (int a = 0; a < NS::NARR; ++a) {

@@ -988,6 +988,11 @@ def gen_function(nest: str, function: str, f32: bool = False) -> Tuple[str, dict
         L.append(f"        case {i}: s.{p.name} = {'(int)iv' if p.ty == 'int' else ('(float)dv' if f32 else 'dv')}; break;")
     L.append("    }")
     L.append("}")
+    try:
+        inner_lo = int(base.bounds[-1][0])
+    except ValueError:
+        inner_lo = -999
+    L.append(f"static constexpr int inner_lo_const = {inner_lo};   // innermost loop's lower bound if constant, else -999")
     L.append("// iteration space: half-open [lo, hi) per marked loop, outermost first")
     L.append("static __host__ __device__ inline void bounds(const Scalars& s, long long lo[NLOOP], long long hi[NLOOP]) {")
     for p in sc:

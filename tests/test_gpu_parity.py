@@ -50,10 +50,9 @@ def to_device(k, name, a, native=True):
     t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
     if not native:
         return t
-    st = k.native_strides(name, tuple(a.shape))
-    if st == tuple(t.stride()):
+    d = backend.empty_native(k, name, tuple(a.shape), t.dtype)   # native strides and start offset
+    if d.stride() == t.stride() and d.storage_offset() == 0:
         return t
-    d = torch.empty_strided(tuple(a.shape), st, dtype=t.dtype, device="cuda")
     backend.copy(d, t)
     return d
 
