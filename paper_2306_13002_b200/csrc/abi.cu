@@ -649,16 +649,16 @@ acs_status acs_native_offset(const acs_kernel* k, const char* array_name, int el
         return ACS_E_ARG;
     }
     *offset_out = 0;
-    // q-major SoA component planes (D3Q19): shift the array by a few elements so
-    // the first interior point of every row (x = the loop's constant lower
-    // bound) starts a 32-byte sector — interior rows then read and write whole
-    // sectors (no over-fetch of the ghost column, no read-modify-write of a
-    // sector shared with it).  Only for the SoA arrays, whose kernels do not
-    // use the TMA (which needs 16-byte-aligned bases).
+    // Shift the array by a few elements so the first interior point of every
+    // row (x = the loop's constant lower bound) starts a 32-byte sector:
+    // interior rows then read and write whole sectors (no over-fetch of the
+    // ghost column, no read-modify-write of a sector shared with it).  Only
+    // for the D3Q19 SoA planes and entries flagged row_offset (zsolve), whose
+    // fast skeletons do not use the TMA (which needs 16-byte-aligned bases).
     bool comp = false;
     for (size_t i = 0; i < e->arrays.size(); ++i)
         if (e->arrays[i] == array_name) comp = e->component_last[i] != 0;
-    if (e->soa_last_dim && comp && e->inner_lo > 0 && 32 % elem_size == 0) {
+    if (((e->soa_last_dim && comp) || e->row_offset) && e->inner_lo > 0 && 32 % elem_size == 0) {
         const int per = 32 / elem_size;
         *offset_out = (per - e->inner_lo % per) % per;
     }

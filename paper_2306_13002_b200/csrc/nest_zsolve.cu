@@ -24,6 +24,7 @@ void register_zsolve() {
     e.kernel_id = "zsolve.c:z_solve_lhs:0";
     e.function = "z_solve_lhs";
     describe<gen::z_solve_lhs>(e, "zsolve.c", 0);
+    e.row_offset = true;   // naive / sliced skeletons only: sector-aligned interior rows
     fill_naive<gen::z_solve_lhs, double>(e, 0);
     fill_zsolve_sliced_a(e);
     fill_zsolve_sliced_b(e);

@@ -49,6 +49,8 @@ struct Entry {
     int best[2][6] = {};         // preferred slot per (precision, variant); acs_tune updates it
     bool soa_last_dim = false;   // backend layout: trailing component subscript made slowest (D3Q19 q)
     int inner_lo = -999;         // the innermost loop's constant lower bound (native row offset)
+    bool row_offset = false;     // native layout: shift real arrays so interior rows are sector-aligned
+                                 // (entries whose fast skeletons do not use the TMA)
     std::vector<int> component_last;  // per array: trailing subscript is an absolute component index
     struct Reach {
         int sliced, loaded, stored, ld_lo, ld_hi, st_lo, st_hi;
