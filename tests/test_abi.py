@@ -93,3 +93,22 @@ def test_cpp_host_api_compiles():
                         "-I", "/usr/local/cuda/include", os.path.join(root, "tests", "cpp", "host_api_check.cpp")],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.parametrize("kid,name,esize,want", [
+    ("d3q19.c:stream_collide:0", "src", 8, 3), ("d3q19.c:stream_collide:0", "dst", 8, 3),
+    ("d3q19.c:stream_collide:0", "flags", 4, 0), ("zsolve.c:z_solve_lhs:0", "lhsZ", 8, 3),
+    ("zsolve.c:z_solve_lhs:0", "fjacZ", 8, 3), ("jacobi7.c:jacobi7:0", "A0", 8, 0),
+    ("wave4.c:wave4:0", "u", 4, 0)])
+def test_native_offset(kid, name, esize, want):
+    """acs_native_offset: SoA planes (D3Q19) and row_offset entries (zsolve)
+    start so that x = 1 (the first interior point) begins a 32-byte sector;
+    arrays the TMA stages (jacobi, wave4) keep a 16-byte-aligned base."""
+    k = backend.Kernel.lookup(kid)
+    off = ctypes.c_int64(-1)
+    f = backend.lib().acs_native_offset
+    f.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_void_p]
+    assert f(k.handle, name.encode(), esize, ctypes.byref(off)) == 0
+    assert off.value == want
+    if want:
+        assert ((want + 1) * esize) % 32 == 0
