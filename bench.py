@@ -169,7 +169,7 @@ def tune_kernel(kid, size, dtype, variant="accsat"):
     w = nests.workload(kid, size, dtype=dtype)
     k = backend.Kernel.lookup(kid)
     arrs = nests.device_inputs(w, native=True, kernel=k)
-    best, ms = k.tune(arrs, dict(w.scalars), variant, reps=3)
+    best, ms = k.tune(arrs, dict(w.scalars), variant, reps=5)
     name = k.info["schedules"][1 if dtype == "f32" else 0][best]
     del arrs
     torch.cuda.empty_cache()
@@ -270,7 +270,7 @@ def main():
     sc = dict(w.scalars)
     tuned_slot, tuned_ms = (None, {})
     if args.schedule == "default" and args.variant != "original":
-        tuned_slot, tuned_ms = k.tune(arrs, sc, args.variant, reps=3)   # untimed autotune
+        tuned_slot, tuned_ms = k.tune(arrs, sc, args.variant, reps=5)   # untimed autotune
         arrs = nests.device_inputs(w, native=True, kernel=k)            # fresh inputs
     flip = {"f": False}
     launches = {"n": 0}
@@ -342,7 +342,7 @@ def main_sharded(args, rank, ws, local, dist, peak, peak_kind):
     stream = torch.cuda.current_stream()
     tuned = None
     if args.schedule == "default" and args.variant != "original":
-        tuned, _ = sr.k.tune(sr.buf, dict(sr.w.scalars), args.variant, reps=3)   # untimed
+        tuned, _ = sr.k.tune(sr.buf, dict(sr.w.scalars), args.variant, reps=5)   # untimed
         sr.schedule = tuned
         sr.refill()
     torch.cuda.synchronize()
