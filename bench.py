@@ -245,6 +245,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--e2e-chunks", type=int, default=16)
+    ap.add_argument("--workload", default="d3q19", choices=["d3q19", "wave4"],
+                    help="d3q19: BASELINE configs[1] (N>1: weak-scaled z slabs); wave4: configs[4], "
+                         "1024^3 fp32 strong-scaled over N z slabs (SURVEY.md §8e scaling metric)")
     ap.add_argument("--e2e-eager", action="store_true", help="enqueue the e2e call eagerly instead of a CUDA graph")
     ap.add_argument("--e2e-split-d2h", action="store_true", help="two download streams in the e2e pipeline")
     ap.add_argument("--e2e-ramp", action="store_true", help="smaller first/last chunks in the e2e pipeline (measured: no gain)")
@@ -260,6 +263,8 @@ def main():
     from paper_2306_13002_b200 import backend, nests
     rank, ws, local, dist = dist_setup(args)
     peak, peak_kind = load_peaks()
+    if args.workload == "wave4":
+        return main_sharded(args, rank, ws, local, dist, peak, peak_kind)
     if ws > 1:
         return main_sharded(args, rank, ws, local, dist, peak, peak_kind)
     kid = WORKLOAD_KID
@@ -329,16 +334,21 @@ def main():
 
 
 def main_sharded(args, rank, ws, local, dist, peak, peak_kind):
-    """N GPUs: the D3Q19 domain is slab-sharded along z, 256 planes per rank
-    (weak scaling: global grid 256 x 256 x 256N).  Each step every rank
-    computes its slab with the pushes that cross a slab face written straight
-    into the neighbour's distribution array over NVLink (CUDA IPC peer
-    memory, from inside the kernel), ordered by device-side flags."""
+    """N GPUs.  d3q19: the domain is slab-sharded along z, 256 planes per rank
+    (weak scaling: global grid 256 x 256 x 256N); the pushes that cross a slab
+    face are written straight into the neighbour's distribution array.
+    wave4 (--workload wave4, any N): the 1024^3 fp32 grid split into N z
+    slabs (strong scaling); the new boundary planes of `un` are written into
+    the neighbours' halos.  Both over NVLink (CUDA IPC peer memory, from
+    inside the kernel), steps ordered by device-side flags."""
     import torch
     from paper_2306_13002_b200 import backend, nests, shard
-    kid = WORKLOAD_KID
-    size = (args.size * ws, args.size, args.size)
-    sr = shard.SlabRank(kid, size, ws, rank, variant=args.variant, schedule=args.schedule)
+    wave = args.workload == "wave4"
+    kid = "wave4.c:wave4:0" if wave else WORKLOAD_KID
+    gsize = 1024 if args.size == 256 and wave else args.size
+    size = (gsize, gsize, gsize) if wave else (args.size * ws, args.size, args.size)
+    sr = shard.SlabRank(kid, size, ws, rank, dtype="f32" if wave else "f64", variant=args.variant,
+                        schedule=args.schedule)
     stream = torch.cuda.current_stream()
     tuned = None
     if args.schedule == "default" and args.variant != "original":
@@ -346,10 +356,11 @@ def main_sharded(args, rank, ws, local, dist, peak, peak_kind):
         sr.schedule = tuned
         sr.refill()
     torch.cuda.synchronize()
-    exp = [None] * ws
-    dist.all_gather_object(exp, sr.export())
-    sr.connect_ipc(exp[rank - 1] if rank > 0 else None, exp[rank + 1] if rank < ws - 1 else None)
-    dist.barrier()
+    if ws > 1:
+        exp = [None] * ws
+        dist.all_gather_object(exp, sr.export())
+        sr.connect_ipc(exp[rank - 1] if rank > 0 else None, exp[rank + 1] if rank < ws - 1 else None)
+        dist.barrier()
     launches = {"n": 0}
 
     def step():
@@ -363,28 +374,40 @@ def main_sharded(args, rank, ws, local, dist, peak, peak_kind):
     with ClockSampler(local) as clk:
         ms = time_steps(step, args.steps, 0, stream, dist)
     local_bytes = sr.w.algorithmic_bytes
-    value = ws * local_bytes / (ms * 1e-3) / 1e9
+    total_bytes = sr.gw.algorithmic_bytes if wave else ws * local_bytes
+    value = total_bytes / (ms * 1e-3) / 1e9
+    if wave:
+        cfg = {"workload": "seismic wave4 4th-order 3-D wave propagation fp32, one step per step (3-level rotation)",
+               "grid": [gsize] * 3, "per_rank_planes": sr.plan.owned(rank)[1] - sr.plan.owned(rank)[0],
+               "form": args.variant, "schedule": args.schedule, "tuned_slot": tuned,
+               "parallelism": f"z-slab sharding x{ws} (strong scaling), fused peer-memory halo write-through + "
+                              "device flags",
+               "layout": "row-major, padded pitch", "l2": "inputs >> L2 (no flush needed)",
+               "bytes_per_point": sr.w.bytes_per_point}
+    else:
+        cfg = {"workload": "D3Q19 lattice-Boltzmann collide+stream (olbm-like) fp64, one sweep per step",
+               "grid": [args.size, args.size, args.size * ws], "per_rank_grid": [args.size] * 3,
+               "form": args.variant, "schedule": args.schedule, "tuned_slot": tuned,
+               "parallelism": f"z-slab sharding x{ws}, fused peer-memory push exchange + device flags",
+               "layout": "q-major SoA in HBM", "l2": "inputs >> L2 (no flush needed)",
+               "bytes_per_point": sr.w.bytes_per_point}
     out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64",
+           "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+           "scaling": "strong" if wave else "weak", "vs_baseline": None, "dtype": "f32" if wave else "f64",
            "data": "synthetic (seeded SplitMix64, SURVEY.md §8d distributions; generated in HBM)",
-           "config": {"workload": "D3Q19 lattice-Boltzmann collide+stream (olbm-like) fp64, one sweep per step",
-                      "grid": [args.size, args.size, args.size * ws], "per_rank_grid": [args.size] * 3,
-                      "form": args.variant, "schedule": args.schedule, "tuned_slot": tuned,
-                      "parallelism": f"z-slab sharding x{ws}, fused peer-memory push exchange + device flags",
-                      "layout": "q-major SoA in HBM", "l2": "inputs >> L2 (no flush needed)",
-                      "bytes_per_point": sr.w.bytes_per_point},
-           "gpu_launches": launches["n"]}
+           "config": cfg, "gpu_launches": launches["n"]}
     achieved = local_bytes / (ms * 1e-3) / 1e9
     out["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                       "frac": round(achieved / peak, 4), "peak_kind": peak_kind, "traffic": load_traffic("stream_collide"),
-                       "kernel": "stream_collide " + args.variant + " (sharded, per rank)"}
+                       "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                       "traffic": load_traffic("wave4_f32" if wave else "stream_collide"),
+                       "kernel": ("wave4_f32 " if wave else "stream_collide ") + args.variant + " (sharded, per rank)"}
     out["clocks"] = clk.summary()
     if not args.no_e2e:
         out["e2e"] = e2e_sharded(args, sr, dist, ws)
     sr.close()
-    dist.barrier()
-    dist.destroy_process_group()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out))
     return 0
@@ -404,20 +427,23 @@ def e2e_sharded(args, sr, dist, ws):
         host[n].copy_(rm[n])
     torch.cuda.synchronize()
 
+    out_name = sr.w.write_arrays[0]      # the produced array: D3Q19 dst, wave4 un
+
     def step():
         roles = shard.role_buffers(sr.nest, names, sr.step_no)
         for p in names:
             rm[p].copy_(host[p], non_blocking=True)
             backend.copy(sr.buf[roles[p]], rm[p], stream)
         sr.step(stream=stream)
-        backend.copy(rm["dst"], sr.buf[roles["dst"]], stream)
-        host["dst"].copy_(rm["dst"], non_blocking=True)
+        backend.copy(rm[out_name], sr.buf[roles[out_name]], stream)
+        host[out_name].copy_(rm[out_name], non_blocking=True)
 
     steps = max(3, min(args.steps, 10))
     ms = time_steps(step, steps, 2, stream, dist)
     h2d = sum(host[n].numel() * host[n].element_size() for n in names)
-    d2h = host["dst"].numel() * host["dst"].element_size()
-    return {"value": round(ws * sr.w.algorithmic_bytes / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+    d2h = host[out_name].numel() * host[out_name].element_size()
+    total = sr.gw.algorithmic_bytes if args.workload == "wave4" else ws * sr.w.algorithmic_bytes
+    return {"value": round(total / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3), "steps": steps,
             "path": "per rank: pinned host slab (reference AoS) -> H2D -> remap -> sharded acs_launch -> remap -> D2H"}
 

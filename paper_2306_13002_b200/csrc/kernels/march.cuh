@@ -645,7 +645,13 @@ __device__ __forceinline__ void win_rows(M& m, const T* win, bool vec_ok, const 
             if constexpr (NS::NLOOP == 3) pt[1] = y;
             T out[WP::stotal() > 0 ? WP::stotal() : 1];
             const int x0 = m.orgx + lx0;
-            const bool defer = vec_ok && x0 >= xlo0 && x0 + RX <= args.hi[P::X];
+            bool defer = vec_ok && x0 >= xlo0 && x0 + RX <= args.hi[P::X];
+            if (args.sh.enabled) {
+                // write-through to a neighbour happens in the scalar store path:
+                // keep it for planes within reach of the slab faces
+                const long long g = (long long)pt[0] + args.sh.origin;
+                if (g < args.sh.lo_thr + 4 || g >= args.sh.hi_thr - 4) defer = false;
+            }
             win_run<WP, M, NS, FORM, RY, 0, RX>(m, win, out, defer, args, pt, lx0, xlo0, args.hi[P::X]);
             if constexpr (WP::stotal() > 0) {
                 if (defer) {
@@ -714,7 +720,7 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
     using WP = WinPlan<NS, T, LAYOUT, TX, TY, BY, FORM, RX>;
     bool vec_ok = false;
     if constexpr (WP::usable()) {
-        vec_ok = !args.sh.enabled;
+        vec_ok = true;   // sharded: per plane below (planes that forward to a neighbour store scalars)
 #pragma unroll
         for (int r = 0; r < NS::NSROW; ++r) {
             if (!WP::srow_on(r)) continue;

@@ -151,6 +151,10 @@ acs_status bind(const LaunchReq& r, KernelArgs<NS>& ka, bool& empty) {
             ka.sh.dlo[a] = (sd.origin - sd.lo_origin) * ka.arr[a].stride[0];
             ka.sh.dhi[a] = (sd.origin - sd.hi_origin) * ka.arr[a].stride[0];
         }
+        // a slab without neighbours (one rank) runs exactly like a plain launch
+        bool any = false;
+        for (int a = 0; a < NS::NARR; ++a) any = any || ka.sh.peer_lo[a] || ka.sh.peer_hi[a];
+        if (!any) ka.sh.enabled = 0;
     }
     long long lo[NS::NLOOP], hi[NS::NLOOP];
     NS::bounds(ka.s, lo, hi);

@@ -74,6 +74,38 @@ def test_sharded_equals_single_domain(kid, size, dtype, nranks, sched):
     assert np.array_equal(got.view(u), ref.view(u)), f"{kid} x{nranks} {sched}: sharded != single domain"
 
 
+def _slots(kid, prec):
+    k = backend.Kernel.lookup(kid)
+    return [i for i, n in enumerate(k.info["schedules"][prec]) if n]
+
+
+@pytest.mark.parametrize("kid,size,dtype,prec", [("wave4.c:wave4:0", (40, 12, 70), "f32", 1),
+                                                 ("jacobi7.c:jacobi7:0", (36, 9, 37), "f64", 0),
+                                                 ("d3q19.c:stream_collide:0", (24, 7, 20), "f64", 0)])
+def test_sharded_every_slot(kid, size, dtype, prec):
+    """Every registered schedule slot (register windows with deferred vector
+    stores on interior planes included) with 2 slabs thick enough to have
+    planes away from the faces: bit-exact vs the single domain."""
+    torch = _torch()
+    steps = 3
+    w, want = single_domain(kid, size, dtype, steps)
+    for slot in _slots(kid, prec):
+        ranks = [shard.SlabRank(kid, size, 2, r, dtype=dtype, schedule=slot) for r in range(2)]
+        ranks[0].connect_local(None, ranks[1])
+        ranks[1].connect_local(ranks[0], None)
+        streams = [torch.cuda.Stream() for _ in ranks]
+        torch.cuda.synchronize()
+        for _ in range(steps):
+            for sr, st in zip(ranks, streams):
+                sr.step(stream=st)
+        torch.cuda.synchronize()
+        plan = ranks[0].plan
+        got = np.concatenate([to_host(sr.owned_slice(LATEST[w.spec.nest])) for sr in ranks], axis=0)
+        ref = want[plan.glo:plan.ghi]
+        u = np.uint64 if ref.itemsize == 8 else np.uint32
+        assert np.array_equal(got.view(u), ref.view(u)), f"{kid} slot {slot}: sharded != single domain"
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
