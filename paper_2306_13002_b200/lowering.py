@@ -135,6 +135,7 @@ class _Lowerer:
         self.stored = set()
         self.n_fma = self.n_loads = self.n_dyn = 0
         self.capture: Optional[Dict[tuple, str]] = None   # if-conversion: store target -> value var
+        self.capture_pair: Optional[Dict[tuple, str]] = None   # first arm's values (second arm stores)
         self.n_ifc = 0
         self.ifconv = ifconv
         self.plain = plain      # nvcc-default arithmetic: C operators, contraction left to the compiler
@@ -522,7 +523,13 @@ class _Lowerer:
                 val = self.conv(code, t, want)
                 offs = self.ref_offsets(s.lhs)
                 if self.capture is not None:    # if-converted branch: the store becomes a value
-                    out.append(f"{pad}{self.capture[self.target_key(s.lhs)]} = {val};")
+                    key = self.target_key(s.lhs)
+                    out.append(f"{pad}{self.capture[key]} = {val};")
+                    if self.capture_pair is not None:
+                        # second arm: store the selected element right away, so
+                        # its value is not held until the end of the arm
+                        out.append(f"{pad}m.template st<ARR_{arr}, {', '.join(map(str, offs))}>"
+                                   f"(_ifc ? {self.capture_pair[key]} : {self.capture[key]});")
                     return
                 if offs is not None:
                     self.static_stores.add((arr, tuple(offs)))
@@ -665,22 +672,16 @@ class _Lowerer:
         out.append(f"{pad}    const bool _ifc = ({c});")
         for key in targets:
             out.append(f"{pad}    {ty[key]} {names_a[key]}, {names_b[key]};")
-        saved = self.capture
-        self.capture = names_a
-        self.st(s.then_s, ind + 1, out)
-        self.capture = names_b
-        self.st(s.else_s, ind + 1, out)
-        self.capture = saved
-        # the stores, in the then-arm's order, one per element
         for key in targets:
-            arr, offs = key
-            if any(v is not None and v not in self.loop_vars for v, _ in offs):
+            if any(v is not None and v not in self.loop_vars for v, _ in key[1]):
                 raise LowerError("if-conversion target not in loop coordinates")
-            # re-derive the device offsets through ref_offsets' bookkeeping
-            ref = ks.Expr("ref", arr, [_affine_expr(v, o) for v, o in offs])
-            o = self.ref_offsets(ref)
-            out.append(f"{pad}    m.template st<ARR_{arr}, {', '.join(map(str, o))}>"
-                       f"(_ifc ? {names_a[key]} : {names_b[key]});")
+        saved = (self.capture, self.capture_pair)
+        self.capture, self.capture_pair = names_a, None
+        self.st(s.then_s, ind + 1, out)
+        # the second arm stores each element (one select) as soon as it is computed
+        self.capture, self.capture_pair = names_b, names_a
+        self.st(s.else_s, ind + 1, out)
+        self.capture, self.capture_pair = saved
         out.append(f"{pad}}}")
 
     def must_write(self, s: ks.Stmt) -> set:
