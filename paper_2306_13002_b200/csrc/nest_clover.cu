@@ -31,6 +31,8 @@ void register_clover() {
         fill_march<gen::pdv_predict, double, 0, 128, 1, 128, 1, 3>(e, 0);
         fill_march<gen::pdv_predict, double, 0, 128, 1, 64, 1, 3>(e, 0);
         fill_march<gen::pdv_predict, double, 0, 64, 1, 64, 1, 4>(e, 0);
+        fill_march<gen::pdv_predict, double, 0, 128, 1, 128, 1, 5>(e, 0);
+        fill_march<gen::pdv_predict, double, 0, 128, 1, 128, 1, 7>(e, 0);
         register_entry(&e);
     }
     {
@@ -42,6 +44,8 @@ void register_clover() {
         fill_march<gen::advec_cell_x, double, 0, 128, 1, 128, 1, 3>(e, 0);
         fill_march<gen::advec_cell_x, double, 0, 128, 1, 64, 1, 3>(e, 0);
         fill_march<gen::advec_cell_x, double, 0, 64, 1, 64, 1, 4>(e, 0);
+        fill_march<gen::advec_cell_x, double, 0, 128, 1, 128, 1, 5>(e, 0);
+        fill_march<gen::advec_cell_x, double, 0, 128, 1, 128, 1, 7>(e, 0);
         register_entry(&e);
     }
 }

@@ -29,6 +29,8 @@ void register_swim() {
         fill_march<gen::calc2, double, 0, 128, 1, 128, 1, 3>(e, 0);
         fill_march<gen::calc2, double, 0, 128, 1, 64, 1, 3>(e, 0);
         fill_march<gen::calc2, double, 0, 64, 1, 64, 1, 4>(e, 0);
+        fill_march<gen::calc2, double, 0, 128, 1, 128, 1, 5>(e, 0);
+        fill_march<gen::calc2, double, 0, 128, 1, 128, 1, 7>(e, 0);
         fill_march<gen::calc2, double, 0, 128, 1, 64, 1, 3, 2>(e, 0);
         register_entry(&e);
     }
