@@ -540,6 +540,8 @@ def per_kernel_table(peak):
         try:
             row["sat_vs_orig_speedup"] = round(row["accsat/default"]["gbs"] / row["original/naive"]["gbs"], 3)
             row["sat_vs_nvcc_default_speedup"] = round(row["accsat/default"]["gbs"] / row["original-nvcc/naive"]["gbs"], 3)
+            # the saturation effect alone: both forms in the same (naive) skeleton
+            row["sat_vs_orig_same_skeleton"] = round(row["accsat/naive"]["gbs"] / row["original/naive"]["gbs"], 3)
             row["bytes_per_point"] = w.bytes_per_point
         except Exception:
             pass
