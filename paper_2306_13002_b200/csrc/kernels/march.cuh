@@ -869,11 +869,8 @@ acs_status launch_march(const LaunchReq& r) {
     constexpr int D = P::maxspan() + PF;
     constexpr int smem = D * P::slot_bytes() + P::static_bytes() + (D + 1) * 8;
     auto kern = march_kernel<NS, T, FORM, LAYOUT, TX, TY, BX, BY, PF, RX>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr_done{0};
+    set_smem_attr_once(kern, smem, attr_done);
     constexpr int NL = NS::NLOOP;
     const long long xlo0 = ka.lo[NL - 1];
     const long long nx = ka.hi[NL - 1] - (P::ALIGNED ? xlo0 - (((xlo0 % P::V) + P::V) % P::V) : xlo0);

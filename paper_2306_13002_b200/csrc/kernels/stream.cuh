@@ -206,11 +206,8 @@ acs_status launch_stream(const LaunchReq& r) {
     constexpr int NL = NS::NLOOP;
     constexpr int smem = S * P::nslot() * BX * 8;
     auto kern = stream_kernel<NS, T, FORM, BX, S>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr_done{0};
+    set_smem_attr_once(kern, smem, attr_done);
     const long long nx = ka.hi[NL - 1] - ka.lo[NL - 1];
     long long nrows = 1;
     if (NL >= 2) nrows = ka.hi[0] - ka.lo[0];

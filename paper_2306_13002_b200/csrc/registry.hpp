@@ -5,6 +5,7 @@
 #pragma once
 
 #include <array>
+#include <atomic>
 #include <cstdlib>
 
 #include <cuda_runtime.h>
@@ -68,6 +69,20 @@ void register_entry(Entry* e);
 Entry* find_entry(const std::string& id);
 
 inline acs_dtype real_dtype(bool f32) { return f32 ? ACS_F32 : ACS_F64; }
+
+// Opt a kernel into more than 48 KB of dynamic shared memory once per device
+// (function attributes are per device; launches may come from several
+// threads, hence the atomic bitmask).
+template <class K>
+inline void set_smem_attr_once(K kern, int smem, std::atomic<unsigned long long>& done) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ULL << (dev & 63);
+    if (!(done.load(std::memory_order_acquire) & bit)) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        done.fetch_or(bit, std::memory_order_acq_rel);
+    }
+}
 
 // Binds descriptors to KernelArgs<NS>, validating names, ranks, dtypes and
 // the static subscript range of the iteration space (the interpreter's
