@@ -554,17 +554,19 @@ def cpu_threads(args):
 
 
 def run_cpu_steps(w, variant, steps, threads, arrays=None):
+    """Timed steps of the reference's CPU path, buffers rotating like the GPU
+    steps (D3Q19 src <-> dst, wave4 up <- u <- un)."""
     import cpu as oracle_cpu
-    from paper_2306_13002_b200 import nests
+    from paper_2306_13002_b200 import shard
     if arrays is None:
         arrays = host_inputs_via_gpu(w)
+    names = list(arrays)
     ts = []
     for s in range(steps):
-        a = dict(arrays)
-        if s % 2 == 1:
-            a["src"], a["dst"] = arrays["dst"], arrays["src"]
+        roles = shard.role_buffers(w.spec.nest, names, s)
+        a = {p: arrays[roles[p]] for p in names}
         t0 = time.perf_counter()
-        oracle_cpu.run(w.spec, a, w.scalars, variant, threads=threads)
+        oracle_cpu.run(w.spec, a, w.scalars, variant, threads=threads, f32=w.dtype == "f32")
         ts.append(time.perf_counter() - t0)
     return ts, arrays
 
@@ -613,7 +615,10 @@ def reference_arm(args):
     if rank != 0:
         return 0
     from paper_2306_13002_b200 import nests
-    w = nests.workload(WORKLOAD_KID, args.size)
+    wave = args.workload == "wave4"
+    # wave4: a bounded 512^3 sample of the 1024^3 workload (4 x 0.54 GB host arrays)
+    w = nests.workload("wave4.c:wave4:0", 512 if args.size == 256 else min(args.size, 512), dtype="f32") if wave \
+        else nests.workload(WORKLOAD_KID, args.size)
     threads = cpu_threads(args)
     arrays = host_inputs_via_gpu(w)
     run_cpu_steps(w, args.variant, 1, threads, arrays)       # warm-up (first touch)
@@ -622,13 +627,19 @@ def reference_arm(args):
     t = sum(ts) / len(ts)
     v = w.algorithmic_bytes / t / 1e9
     out = {"metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": steps,
-           "warmup": 1, "ms_per_step": round(t * 1e3, 2), "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64, identical inputs)",
+           "warmup": 1, "ms_per_step": round(t * 1e3, 2), "higher_is_better": True,
+           "scaling": "strong" if wave else "weak",
+           "vs_baseline": None, "dtype": "f32" if wave else "f64", "data": "synthetic (seeded SplitMix64, identical inputs)",
            "impl": "reference",
-           "config": {"workload": "D3Q19 lattice-Boltzmann collide+stream (olbm-like) fp64, one sweep per step",
-                      "grid": [args.size] * 3, "form": args.variant},
+           "config": ({"workload": "seismic wave4 4th-order 3-D wave propagation fp32, one step per step "
+                                   "(3-level rotation)", "grid": [1024] * 3,
+                       "form": args.variant} if wave else
+                      {"workload": "D3Q19 lattice-Boltzmann collide+stream (olbm-like) fp64, one sweep per step",
+                       "grid": [args.size] * 3, "form": args.variant}),
            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-                            "sample": f"{steps} full sweeps; reference-emitted {args.variant} C compiled by gcc "
+                            "sample": (f"{steps} steps on a {round(w.points ** (1 / 3))}^3 sample" if wave
+                                       else f"{steps} full sweeps") +
+                                      f"; reference-emitted {args.variant} C compiled by gcc "
                                       "-O3 -ffp-contract=off (satcc wrapper mode), OpenMP over z",
                             "cpu": cpu_model()},
            "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
