@@ -419,7 +419,14 @@ def main_sharded(args, rank, ws, local, dist, peak, peak_kind):
                        "kernel": ("wave4_f32 " if wave else "stream_collide ") + args.variant + " (sharded, per rank)"}
     out["clocks"] = clk.summary()
     if not args.no_e2e:
-        out["e2e"] = e2e_sharded(args, sr, dist, ws)
+        if ws == 1:
+            # one slab: the overlapped host-buffer pipeline (as for the D3Q19 line)
+            sr.close()
+            del sr.buf
+            torch.cuda.empty_cache()
+            out["e2e"] = e2e_d3q19(args, sr.gw, sr.k, dist)
+        else:
+            out["e2e"] = e2e_sharded(args, sr, dist, ws)
     sr.close()
     if dist:
         dist.barrier()
