@@ -161,6 +161,10 @@ struct MarchPlan {
 template <class NS>
 struct TmaMaps {
     CUtensorMap m[NS::NARR];
+    // x-origin shift of each tensor map (elements): an array whose data pointer
+    // is not 16-byte aligned (a sector-aligned native row offset) is described
+    // from the aligned address adj elements earlier, its x coordinates + adj
+    int adj[NS::NARR];
 };
 
 // per-CTA state a body's memory policy needs
@@ -547,7 +551,8 @@ __device__ __forceinline__ void march_issue(unsigned char* slot_base, const TmaM
                     const int p = P::pos_of_dim(A, d);
                     const int s = NS::ld_sig(A, p);
                     if (s == 0) c[d] = plane_base + NS::ld_hi(A, p);
-                    else if (s == P::X) c[d] = orgx + P::lo(A, p) - (d == 0 ? xshift<P, NS>(A, orgx) : 0);
+                    else if (s == P::X)
+                        c[d] = orgx + maps.adj[A] + P::lo(A, p) - (d == 0 ? xshift<P, NS>(A, orgx + maps.adj[A]) : 0);
                     else if (s == P::Y) c[d] = orgy + NS::ld_lo(A, p);
                     else c[d] = NS::ld_lo(A, p);
                 }
@@ -714,7 +719,7 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
     bool aligned = true;
 #pragma unroll
     for (int a = 0; a < NS::NARR; ++a) {
-        m.sh[a] = xshift<P, NS>(a, orgx);
+        m.sh[a] = xshift<P, NS>(a, orgx + maps.adj[a]);
         if (P::staged(a) && m.sh[a] != 0) aligned = false;
     }
     using WP = WinPlan<NS, T, LAYOUT, TX, TY, BY, FORM, RX>;
@@ -812,7 +817,11 @@ bool encode_maps(const LaunchReq& r, TmaMaps<NS>& maps) {
             acc *= d->dims[p];
         }
         const int es = P::esize(a);
-        if (reinterpret_cast<uintptr_t>(d->data) % 16 != 0) ACS_TMA_FAIL("base not 16-byte aligned");
+        const int mis = (int)(reinterpret_cast<uintptr_t>(d->data) % 16);
+        if (mis % es != 0) ACS_TMA_FAIL("base not element aligned");
+        const int adj = mis / es;
+        if (adj && (P::ALIGNED || !P::inner_is_x(a))) ACS_TMA_FAIL("unaligned base on the aligned-origin path");
+        maps.adj[a] = adj;
         cuuint64_t gdim[5], gstr[4];
         cuuint32_t box[5], estr[5];
         long long prev = 0;
@@ -824,14 +833,15 @@ bool encode_maps(const LaunchReq& r, TmaMaps<NS>& maps) {
                 gstr[dd - 1] = (cuuint64_t)(st[p] * es);
             }
             prev = st[p];
-            gdim[dd] = (cuuint64_t)d->dims[p];
+            gdim[dd] = (cuuint64_t)(d->dims[p] + (dd == 0 ? adj : 0));
             box[dd] = (cuuint32_t)P::extent(a, p);
             estr[dd] = 1;
         }
         const CUtensorMapDataType dt = NS::is_int(a) ? CU_TENSOR_MAP_DATA_TYPE_INT32
                                        : sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
                                                         : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-        CUresult e = enc(&maps.m[a], dt, (cuuint32_t)nd, d->data, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        void* base = static_cast<char*>(d->data) - (size_t)adj * es;
+        CUresult e = enc(&maps.m[a], dt, (cuuint32_t)nd, base, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (acs_debug()) {

@@ -11,6 +11,7 @@ void register_jacobi7() {
         e.kernel_id = "jacobi7.c:jacobi7:0";
         e.function = "jacobi7";
         describe<gen::jacobi7>(e, "jacobi7.c", 0);
+        e.row_offset = true;   // sector-aligned rows; the TMA maps start adj elements earlier
         fill_naive<gen::jacobi7, double>(e, 0);
         fill_march<gen::jacobi7, double, 0, 64, 4, 64, 4, 3>(e, 0);
         fill_march<gen::jacobi7, double, 0, 128, 4, 128, 2, 5>(e, 0);
