@@ -161,6 +161,7 @@ struct MarchPlan {
 template <class NS>
 struct TmaMaps {
     CUtensorMap m[NS::NARR];
+    int adjx;   // the common adj of the staged arrays (aligned-origin path)
     // x-origin shift of each tensor map (elements): an array whose data pointer
     // is not 16-byte aligned (a sector-aligned native row offset) is described
     // from the aligned address adj elements earlier, its x coordinates + adj
@@ -686,7 +687,8 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * BX + tx;
     const int xlo0 = (int)args.lo[P::X];
-    const int orgx = (P::ALIGNED ? xlo0 - (((xlo0 % P::V) + P::V) % P::V) : xlo0) + blockIdx.x * TX;
+    // aligned origin: orgx + adj (the tensor-map x coordinate) is a multiple of V
+    const int orgx = (P::ALIGNED ? xlo0 - ((((xlo0 + maps.adjx) % P::V) + P::V) % P::V) : xlo0) + blockIdx.x * TX;
     const int orgy = NS::NLOOP == 3 ? args.lo[1] + blockIdx.y * TY : 0;
     const int kb = args.lo[0] + blockIdx.z * kchunk;
     const int ke = min(kb + kchunk, args.hi[0]);
@@ -730,7 +732,8 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
         for (int r = 0; r < NS::NSROW; ++r) {
             if (!WP::srow_on(r)) continue;
             const int a = NS::srow_arr(r);
-            if (reinterpret_cast<uintptr_t>(args.arr[a].base) % 16 != 0) vec_ok = false;
+            // the point group's first element must be 16-byte aligned
+            if ((reinterpret_cast<uintptr_t>(args.arr[a].base) + (uintptr_t)orgx * sizeof(T)) % 16 != 0) vec_ok = false;
             for (int p = 0; p < NS::ndim(a); ++p) {
                 const long long st = args.arr[a].stride[p];
                 if (p == WP::sxpos(a) ? st != 1 : st % WP::V != 0) vec_ok = false;
@@ -797,6 +800,7 @@ template <class NS, class T, int LAYOUT, int TX, int TY, int RX = 1>
 bool encode_maps(const LaunchReq& r, TmaMaps<NS>& maps) {
     using P = MarchPlan<NS, T, LAYOUT, TX, TY, RX>;
     EncodeTiledFn enc = tma_encoder();
+    bool first_staged = true;
     if (!enc) {
         if (acs_debug()) std::fprintf(stderr, "[acs] no cuTensorMapEncodeTiled entry point\n");
         return false;
@@ -820,7 +824,12 @@ bool encode_maps(const LaunchReq& r, TmaMaps<NS>& maps) {
         const int mis = (int)(reinterpret_cast<uintptr_t>(d->data) % 16);
         if (mis % es != 0) ACS_TMA_FAIL("base not element aligned");
         const int adj = mis / es;
-        if (adj && (P::ALIGNED || !P::inner_is_x(a))) ACS_TMA_FAIL("unaligned base on the aligned-origin path");
+        if (adj && !P::inner_is_x(a)) ACS_TMA_FAIL("unaligned base of an array whose innermost subscript is not x");
+        if (P::ALIGNED) {   // one shared origin: every staged array must have the same shift
+            if (first_staged) maps.adjx = adj;
+            else if (maps.adjx != adj) ACS_TMA_FAIL("staged arrays with different base shifts");
+            first_staged = false;
+        }
         maps.adj[a] = adj;
         cuuint64_t gdim[5], gstr[4];
         cuuint32_t box[5], estr[5];
@@ -883,7 +892,7 @@ acs_status launch_march(const LaunchReq& r) {
     set_smem_attr_once(kern, smem, attr_done);
     constexpr int NL = NS::NLOOP;
     const long long xlo0 = ka.lo[NL - 1];
-    const long long nx = ka.hi[NL - 1] - (P::ALIGNED ? xlo0 - (((xlo0 % P::V) + P::V) % P::V) : xlo0);
+    const long long nx = ka.hi[NL - 1] - (P::ALIGNED ? xlo0 - ((((xlo0 + maps.adjx) % P::V) + P::V) % P::V) : xlo0);
     const long long ny = NL == 3 ? ka.hi[1] - ka.lo[1] : 1;
     const long long nz = ka.hi[0] - ka.lo[0];
     const long long tiles = ((nx + TX - 1) / TX) * (NL == 3 ? (ny + TY - 1) / TY : 1);

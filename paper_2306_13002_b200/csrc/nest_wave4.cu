@@ -11,6 +11,7 @@ void register_wave4() {
         e.kernel_id = "wave4.c:wave4:0";
         e.function = "wave4";
         describe<gen::wave4>(e, "wave4.c", 0);
+        e.row_offset = true;   // sector-aligned rows (TMA x-origin shift, aligned origin follows it)
         fill_naive<gen::wave4, double>(e, 0);
         fill_march<gen::wave4, double, 0, 32, 8, 32, 8, 3>(e, 0);
         fill_march<gen::wave4, double, 0, 32, 16, 32, 4, 3>(e, 0);

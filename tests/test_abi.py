@@ -99,12 +99,12 @@ def test_cpp_host_api_compiles():
     ("d3q19.c:stream_collide:0", "src", 8, 3), ("d3q19.c:stream_collide:0", "dst", 8, 3),
     ("d3q19.c:stream_collide:0", "flags", 4, 0), ("zsolve.c:z_solve_lhs:0", "lhsZ", 8, 3),
     ("zsolve.c:z_solve_lhs:0", "fjacZ", 8, 3), ("jacobi7.c:jacobi7:0", "A0", 8, 3),
-    ("wave4.c:wave4:0", "u", 4, 0)])
+    ("wave4.c:wave4:0", "u", 4, 6)])
 def test_native_offset(kid, name, esize, want):
     """acs_native_offset: SoA planes (D3Q19) and row_offset entries (zsolve)
     start so that x = 1 (the first interior point) begins a 32-byte sector;
-    jacobi too (its TMA maps start adj elements earlier); wave4 keeps a 16-byte-aligned
-    base for its aligned-origin register-window path."""
+    jacobi and wave4 too (their TMA maps start adj elements earlier; wave4's
+    aligned register-window origin follows the shift)."""
     k = backend.Kernel.lookup(kid)
     off = ctypes.c_int64(-1)
     f = backend.lib().acs_native_offset
