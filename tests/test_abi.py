@@ -112,4 +112,5 @@ def test_native_offset(kid, name, esize, want):
     assert f(k.handle, name.encode(), esize, ctypes.byref(off)) == 0
     assert off.value == want
     if want:
-        assert ((want + 1) * esize) % 32 == 0
+        lo = 2 if kid.startswith("wave4") else 1     # the innermost loop's first interior point
+        assert ((want + lo) * esize) % 32 == 0
