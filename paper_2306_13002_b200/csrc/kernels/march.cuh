@@ -161,11 +161,11 @@ struct MarchPlan {
 template <class NS>
 struct TmaMaps {
     CUtensorMap m[NS::NARR];
-    int adjx;   // the common adj of the staged arrays (aligned-origin path)
-    // x-origin shift of each tensor map (elements): an array whose data pointer
-    // is not 16-byte aligned (a sector-aligned native row offset) is described
-    // from the aligned address adj elements earlier, its x coordinates + adj
-    int adj[NS::NARR];
+    // x-origin shift of the tensor maps (elements, the same for every staged
+    // array): an array whose data pointer is not 16-byte aligned (a
+    // sector-aligned native row offset) is described from the aligned address
+    // adjx elements earlier, so its tensor x coordinate is x + adjx
+    int adjx;
 };
 
 // per-CTA state a body's memory policy needs
@@ -553,7 +553,7 @@ __device__ __forceinline__ void march_issue(unsigned char* slot_base, const TmaM
                     const int s = NS::ld_sig(A, p);
                     if (s == 0) c[d] = plane_base + NS::ld_hi(A, p);
                     else if (s == P::X)
-                        c[d] = orgx + maps.adj[A] + P::lo(A, p) - (d == 0 ? xshift<P, NS>(A, orgx + maps.adj[A]) : 0);
+                        c[d] = orgx + P::lo(A, p) - (d == 0 ? xshift<P, NS>(A, orgx) : 0);
                     else if (s == P::Y) c[d] = orgy + NS::ld_lo(A, p);
                     else c[d] = NS::ld_lo(A, p);
                 }
@@ -703,11 +703,11 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
     if (tid == 0) {
         if constexpr (P::static_tx() > 0) {
             mbar_expect_tx(&bars[D], P::static_tx());
-            march_issue<P, NS, 0>(nullptr, maps, &bars[D], 0, orgx, orgy, true, stat);
+            march_issue<P, NS, 0>(nullptr, maps, &bars[D], 0, orgx + maps.adjx, orgy, true, stat);
         }
         for (int B = 0; B < D - 1 && B < nb; ++B) {
             mbar_expect_tx(&bars[B % D], P::slot_tx());
-            march_issue<P, NS, 0>(ring + (B % D) * P::slot_bytes(), maps, &bars[B % D], kb + B - (MS - 1), orgx,
+            march_issue<P, NS, 0>(ring + (B % D) * P::slot_bytes(), maps, &bars[B % D], kb + B - (MS - 1), orgx + maps.adjx,
                                   orgy, false, stat);
         }
     }
@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
     bool aligned = true;
 #pragma unroll
     for (int a = 0; a < NS::NARR; ++a) {
-        m.sh[a] = xshift<P, NS>(a, orgx + maps.adj[a]);
+        m.sh[a] = xshift<P, NS>(a, orgx + maps.adjx);
         if (P::staged(a) && m.sh[a] != 0) aligned = false;
     }
     using WP = WinPlan<NS, T, LAYOUT, TX, TY, BY, FORM, RX>;
@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
                 fence_proxy_async();
                 mbar_expect_tx(&bars[B % D], P::slot_tx());
                 march_issue<P, NS, 0>(ring + (B % D) * P::slot_bytes(), maps, &bars[B % D], kb + B - (MS - 1),
-                                      orgx, orgy, false, stat);
+                                      orgx + maps.adjx, orgy, false, stat);
             }
         }
         const int Bw = s + MS - 1;
@@ -825,12 +825,10 @@ bool encode_maps(const LaunchReq& r, TmaMaps<NS>& maps) {
         if (mis % es != 0) ACS_TMA_FAIL("base not element aligned");
         const int adj = mis / es;
         if (adj && !P::inner_is_x(a)) ACS_TMA_FAIL("unaligned base of an array whose innermost subscript is not x");
-        if (P::ALIGNED) {   // one shared origin: every staged array must have the same shift
-            if (first_staged) maps.adjx = adj;
-            else if (maps.adjx != adj) ACS_TMA_FAIL("staged arrays with different base shifts");
-            first_staged = false;
-        }
-        maps.adj[a] = adj;
+        // one shared shift: the kernel works in tensor-map x coordinates (x + adjx)
+        if (first_staged) maps.adjx = adj;
+        else if (maps.adjx != adj) ACS_TMA_FAIL("staged arrays with different base shifts");
+        first_staged = false;
         cuuint64_t gdim[5], gstr[4];
         cuuint32_t box[5], estr[5];
         long long prev = 0;

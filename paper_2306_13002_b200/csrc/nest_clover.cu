@@ -12,6 +12,7 @@ void register_clover() {
         e.kernel_id = "clover.c:ideal_gas:0";
         e.function = "ideal_gas";
         describe<gen::ideal_gas>(e, "clover.c", 0);
+        e.row_offset = true;   // sector-aligned rows (x starts at 2: a 16-byte shift)
         fill_naive<gen::ideal_gas, double>(e, 0);
         fill_naive_multi<gen::ideal_gas, double, 2>(e, 0);
         fill_naive_multi<gen::ideal_gas, double, 4>(e, 0);
