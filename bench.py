@@ -540,7 +540,7 @@ def per_kernel_table(peak):
         for variant, sched in (("original", "naive"), ("original-nvcc", "naive"), ("accsat", "naive"),
                                ("accsat", "default")):
             try:
-                ms, gbs, w = bench_kernel(kid, size, dtype, sweeps, variant, sched, reps=3 if sweeps > 1 else 5)
+                ms, gbs, w = bench_kernel(kid, size, dtype, sweeps, variant, sched, reps=5)
                 row[f"{variant}/{sched}"] = {"ms": round(ms, 4), "gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
             except Exception as e:  # report, never hide
                 row[f"{variant}/{sched}"] = {"error": str(e)[:200]}
