@@ -171,7 +171,7 @@ __device__ __forceinline__ void q_step(const G& g, T* q, bool first) {
 
 // the k march of one slice, the slice a compile-time constant: no switch in
 // the loop, so the loads of several planes can be issued ahead (unroll)
-template <class NS, class T, int FORM, int S>
+template <class NS, class T, int FORM, int S, int UNR>
 __device__ __forceinline__ void march_slice(NaiveMem<NS, T, FORM == ACS_ORIGINAL>& m, const KernelArgs<NS>& args,
                                             int* pt, int slice, int kb, int ke) {
     if constexpr (S < NS::nslices[FORM]) {
@@ -188,7 +188,7 @@ __device__ __forceinline__ void march_slice(NaiveMem<NS, T, FORM == ACS_ORIGINAL
                 }
                 // steady state: straight-line shift + one load per queue, so the
                 // unrolled planes' loads can all be issued ahead
-#pragma unroll 4
+#pragma unroll UNR
                 for (int k = kb + 1; k < ke; ++k) {
                     pt[0] = k;
                     q_step<NS, QP, G, T, 0>(m, q, false);
@@ -196,19 +196,19 @@ __device__ __forceinline__ void march_slice(NaiveMem<NS, T, FORM == ACS_ORIGINAL
                     NS::template body_slice<FORM, S>(qm, args.s, pt);
                 }
             } else {
-#pragma unroll 4
+#pragma unroll UNR
                 for (int k = kb; k < ke; ++k) {
                     pt[0] = k;
                     NS::template body_slice<FORM, S>(m, args.s, pt);
                 }
             }
         } else {
-            march_slice<NS, T, FORM, S + 1>(m, args, pt, slice, kb, ke);
+            march_slice<NS, T, FORM, S + 1, UNR>(m, args, pt, slice, kb, ke);
         }
     }
 }
 
-template <class NS, class T, int FORM, int BX, int BY>
+template <class NS, class T, int FORM, int BX, int BY, int UNR>
 __global__ void __launch_bounds__(BX* BY) sliced_kernel(const __grid_constant__ KernelArgs<NS> args, int kchunk) {
     static_assert(NS::NLOOP == 3, "sliced skeleton: 3-D nests");
     constexpr int NSL = NS::nslices[FORM];
@@ -227,11 +227,11 @@ __global__ void __launch_bounds__(BX* BY) sliced_kernel(const __grid_constant__ 
     pt[1] = y;
     pt[2] = x;
     NaiveMem<NS, T, FORM == ACS_ORIGINAL> m{args, pt};
-    march_slice<NS, T, FORM, 0>(m, args, pt, slice, kb, ke);
+    march_slice<NS, T, FORM, 0, UNR>(m, args, pt, slice, kb, ke);
     if (args.sh.enabled) __threadfence_system();   // peer write-through visible before the step flag
 }
 
-template <class NS, class T, int FORM, int BX, int BY, int KCH>
+template <class NS, class T, int FORM, int BX, int BY, int KCH, int UNR>
 acs_status launch_sliced(const LaunchReq& r) {
     KernelArgs<NS> ka;
     bool empty = false;
@@ -242,20 +242,21 @@ acs_status launch_sliced(const LaunchReq& r) {
     const long long nx = ka.hi[2] - x0, ny = ka.hi[1] - ka.lo[1], nz = ka.hi[0] - ka.lo[0];
     const long long chunks = (nz + KCH - 1) / KCH;
     dim3 grid((unsigned)((nx + BX - 1) / BX), (unsigned)((ny + BY - 1) / BY), (unsigned)(chunks * NSL));
-    sliced_kernel<NS, T, FORM, BX, BY><<<grid, dim3(BX, BY, 1), 0, r.stream>>>(ka, KCH);
+    sliced_kernel<NS, T, FORM, BX, BY, UNR><<<grid, dim3(BX, BY, 1), 0, r.stream>>>(ka, KCH);
     return check_launch("sliced");
 }
 
-template <class NS, class T, int BX, int BY, int KCH>
+template <class NS, class T, int BX, int BY, int KCH, int UNR = 4>
 void fill_sliced(Entry& e, int prec) {
     const int slot = e.n_sched[prec]++;
-    e.launch[prec][0][slot] = &launch_sliced<NS, T, 0, BX, BY, KCH>;
-    e.launch[prec][1][slot] = &launch_sliced<NS, T, 1, BX, BY, KCH>;
-    e.launch[prec][2][slot] = &launch_sliced<NS, T, 2, BX, BY, KCH>;
-    e.launch[prec][3][slot] = &launch_sliced<NS, T, 3, BX, BY, KCH>;
-    e.launch[prec][4][slot] = &launch_sliced<NS, T, 4, BX, BY, KCH>;
+    e.launch[prec][0][slot] = &launch_sliced<NS, T, 0, BX, BY, KCH, UNR>;
+    e.launch[prec][1][slot] = &launch_sliced<NS, T, 1, BX, BY, KCH, UNR>;
+    e.launch[prec][2][slot] = &launch_sliced<NS, T, 2, BX, BY, KCH, UNR>;
+    e.launch[prec][3][slot] = &launch_sliced<NS, T, 3, BX, BY, KCH, UNR>;
+    e.launch[prec][4][slot] = &launch_sliced<NS, T, 4, BX, BY, KCH, UNR>;
     e.sched_name[prec][slot] = "sliced " + std::to_string(NS::nslices[4]) + " components, block " +
-                               std::to_string(BX) + "x" + std::to_string(BY) + ", k-chunk " + std::to_string(KCH);
+                               std::to_string(BX) + "x" + std::to_string(BY) + ", k-chunk " + std::to_string(KCH) +
+                               ", unroll " + std::to_string(UNR);
     for (int v = 0; v < 5; ++v)
         if (e.best[prec][v] == 0 && v != ACS_ORIGINAL) e.best[prec][v] = slot;
 }
