@@ -597,9 +597,11 @@ def host_inputs_via_gpu(w):
 
 def cpu_baseline(w, args):
     threads = cpu_threads(args)
-    ts, _ = run_cpu_steps(w, "accsat", 3, threads)
+    ts, arrays = run_cpu_steps(w, "accsat", 3, threads)
     t = float(np.median(ts))
+    t1, _ = run_cpu_steps(w, "accsat", 1, 1, arrays)      # one core, one sweep
     return {"value": round(w.algorithmic_bytes / t / 1e9, 3), "unit": "GB/s", "cores": threads,
+            "value_1core": round(w.algorithmic_bytes / t1[0] / 1e9, 3),
             "kind": "reference",
             "sample": f"3 full {w.dims['flags']} D3Q19 sweeps of the reference-emitted accsat C "
                       f"(gcc -O3 -ffp-contract=off, OpenMP over z), median",
