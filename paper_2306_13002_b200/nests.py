@@ -188,7 +188,8 @@ def workload(kernel_id: str, size=None, dtype: str = "f64") -> Workload:
         sc = {"omega": 1.95, "zbeg": 1, "zend": nz + 1, "ny": d[1], "nx": d[2]}
         fills = {"src": Fill("d3q19", -0.01, 0.01), "dst": Fill("d3q19", -0.01, 0.01),
                  "flags": Fill("mask", p=0.1)}
-        # 19 reads + 19 writes of 8 B + the 1-byte flag (uint8 on the device)
+        # 19 reads + 19 writes of 8 B + the 1-byte flag of SURVEY §8d (the device keeps the
+        # nest's int32 flags, so 3 B/point moved are not credited — DESIGN Next 2)
         return Workload(s, dims, sc, fills, "f64", nz * ny * nx, 19 * 8 * 2 + 1,
                         ["src", "flags"], ["dst"])
     if s.nest == "swim":

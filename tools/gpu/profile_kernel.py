@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Runs one nest at its BASELINE size a few times (for ncu captures):
-   python tools/gpu/profile_kernel.py <kernel_id> <variant> <schedule> [f32] [reps]"""
+   python tools/gpu/profile_kernel.py <kernel_id> <variant> <schedule|tuned> [f32] [reps]"""
 import os
 import sys
 
@@ -16,6 +16,10 @@ reps = int(sys.argv[5]) if len(sys.argv) > 5 else 4
 w = nests.workload(kid, None, dtype=dtype)
 k = backend.Kernel.lookup(kid)
 arrs = nests.device_inputs(w, native=True, kernel=k)
+if sched == "tuned":                       # print the tuner's choice (as a profile_kernel slot) and exit
+    best, _ = k.tune(arrs, dict(w.scalars), variant)
+    print(best + 16 if best > 0 else "naive")
+    sys.exit(0)
 torch.cuda.synchronize()
 for _ in range(reps):
     k.launch(arrs, dict(w.scalars), variant, sched)
