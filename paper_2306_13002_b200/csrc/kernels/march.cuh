@@ -868,7 +868,7 @@ bool encode_maps(const LaunchReq& r, TmaMaps<NS>& maps) {
     return true;
 }
 
-template <class NS, class T, int FORM, int LAYOUT, int TX, int TY, int BX, int BY, int PF, int RX = 1>
+template <class NS, class T, int FORM, int LAYOUT, int TX, int TY, int BX, int BY, int PF, int RX = 1, int KCH = 0>
 acs_status launch_march(const LaunchReq& r) {
     using P = MarchPlan<NS, T, LAYOUT, TX, TY, RX>;
     static_assert(P::usable(), "march skeleton: nest not stageable");
@@ -899,6 +899,12 @@ acs_status launch_march(const LaunchReq& r) {
     long long kchunk = (nz + want - 1) / want;
     const long long minch = 4LL * (P::maxspan() > 1 ? P::maxspan() : 2);
     if (kchunk < minch) kchunk = minch;
+    static const long long kch_env = [] {   // experiment knob (tools/gpu), not a tuning path
+        const char* e = std::getenv("ACS_MARCH_KCHUNK");
+        return e ? std::atoll(e) : 0LL;
+    }();
+    if (KCH > 0) kchunk = KCH;                // registered one-wave configurations
+    else if (kch_env > 0) kchunk = kch_env;
     if (kchunk > nz) kchunk = nz;
     const long long chunks = (nz + kchunk - 1) / kchunk;
     dim3 grid((unsigned)((nx + TX - 1) / TX), (unsigned)(NL == 3 ? (ny + TY - 1) / TY : 1), (unsigned)chunks);
@@ -906,17 +912,18 @@ acs_status launch_march(const LaunchReq& r) {
     return check_launch("march");
 }
 
-template <class NS, class T, int LAYOUT, int TX, int TY, int BX, int BY, int PF, int RX = 1>
+template <class NS, class T, int LAYOUT, int TX, int TY, int BX, int BY, int PF, int RX = 1, int KCH = 0>
 void fill_march(Entry& e, int prec) {
     const int slot = e.n_sched[prec]++;
-    e.launch[prec][0][slot] = &launch_march<NS, T, 0, LAYOUT, TX, TY, BX, BY, PF, RX>;
-    e.launch[prec][1][slot] = &launch_march<NS, T, 1, LAYOUT, TX, TY, BX, BY, PF, RX>;
-    e.launch[prec][2][slot] = &launch_march<NS, T, 2, LAYOUT, TX, TY, BX, BY, PF, RX>;
-    e.launch[prec][3][slot] = &launch_march<NS, T, 3, LAYOUT, TX, TY, BX, BY, PF, RX>;
-    e.launch[prec][4][slot] = &launch_march<NS, T, 4, LAYOUT, TX, TY, BX, BY, PF, RX>;
+    e.launch[prec][0][slot] = &launch_march<NS, T, 0, LAYOUT, TX, TY, BX, BY, PF, RX, KCH>;
+    e.launch[prec][1][slot] = &launch_march<NS, T, 1, LAYOUT, TX, TY, BX, BY, PF, RX, KCH>;
+    e.launch[prec][2][slot] = &launch_march<NS, T, 2, LAYOUT, TX, TY, BX, BY, PF, RX, KCH>;
+    e.launch[prec][3][slot] = &launch_march<NS, T, 3, LAYOUT, TX, TY, BX, BY, PF, RX, KCH>;
+    e.launch[prec][4][slot] = &launch_march<NS, T, 4, LAYOUT, TX, TY, BX, BY, PF, RX, KCH>;
     e.sched_name[prec][slot] = "march tile " + std::to_string(TX) + "x" + std::to_string(TY) + " block " +
                                std::to_string(BX) + "x" + std::to_string(BY) + " pf " + std::to_string(PF) +
-                               (RX > 1 ? " regwin " + std::to_string(RX) : "");
+                               (RX > 1 ? " regwin " + std::to_string(RX) : "") +
+                               (KCH > 0 ? " k-chunk " + std::to_string(KCH) : "");
     for (int v = 0; v < 5; ++v)
         if (e.best[prec][v] == 0 && v != ACS_ORIGINAL) e.best[prec][v] = slot;
 }

@@ -50,11 +50,15 @@ struct QPlan {
         return -1;
     }
     static constexpr bool eligible(int i) {
-        const int a = NS::sl_arr(i), mp = mpos(a);
-        if (FORM == 0 || mp < 0 || !NS::readonly(a) || NS::is_int(a)) return false;
-        for (int p = 0; p < NS::ndim(a); ++p)
-            if (NS::sig(a, p) > 0 && NS::sl_off(i, p) != 0) return false;
-        return true;
+        if constexpr (FORM == 0) {
+            return false;
+        } else {
+            const int a = NS::sl_arr(i), mp = mpos(a);
+            if (mp < 0 || !NS::readonly(a) || NS::is_int(a)) return false;
+            for (int p = 0; p < NS::ndim(a); ++p)
+                if (NS::sig(a, p) > 0 && NS::sl_off(i, p) != 0) return false;
+            return true;
+        }
     }
     static constexpr bool same_field(int i, int j) {
         const int a = NS::sl_arr(i);
