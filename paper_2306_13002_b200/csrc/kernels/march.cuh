@@ -898,7 +898,9 @@ acs_status launch_march(const LaunchReq& r) {
     const long long want = (148LL * 4 * 8 + tiles - 1) / tiles;
     long long kchunk = (nz + want - 1) / want;
     const long long minch = 4LL * (P::maxspan() > 1 ? P::maxspan() : 2);
-    if (kchunk < minch) kchunk = minch;
+    // 2-D row strips: the shortest chunk the prologue allows (measured, tools/gpu/kchunk_sweep.sh:
+    // calc2 6381 -> 6988 GB/s, pdv 6572 -> 6806 against ~100-row chunks); 3-D keeps ~8 waves
+    if (NL == 2 || kchunk < minch) kchunk = minch;
     static const long long kch_env = [] {   // experiment knob (tools/gpu), not a tuning path
         const char* e = std::getenv("ACS_MARCH_KCHUNK");
         return e ? std::atoll(e) : 0LL;

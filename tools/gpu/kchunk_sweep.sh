@@ -2,7 +2,7 @@
 # per march nest: bash tools/gpu/kchunk_sweep.sh > gpurun_out/kchunk.log
 mkdir -p gpurun_out
 one() {  # kid size dtype sweeps
-  for K in 0 8 16 24 32 48 64; do
+  for K in ${KS:-0 8 16 24 32 48 64}; do
     ACS_MARCH_KCHUNK=$K timeout 600 python - "$1" "$2" "$3" "$4" "$K" <<'PY'
 import json, sys, bench
 kid, size, dt, sw, K = sys.argv[1], int(sys.argv[2]), sys.argv[3], int(sys.argv[4]), sys.argv[5]
@@ -13,6 +13,12 @@ print(json.dumps({"kid": kid, "kchunk": K, "slot": slot, "name": name, "gbs": ro
 PY
   done
 }
+if [ "$1" = 2d ]; then   # the 2-D nests around the launcher's minimum chunk
+  KS="0 4 6 12"
+  for k in swim.c:calc1:0 swim.c:calc2:1; do one $k 8192 f64 1; done
+  for k in clover.c:ideal_gas:0 clover.c:pdv_predict:1 clover.c:advec_cell_x:2; do one $k 7680 f64 1; done
+  exit 0
+fi
 one jacobi7.c:jacobi7:0 256 f64 100
 one wave4.c:wave4:0 1024 f32 1
 one clover.c:pdv_predict:1 7680 f64 1
