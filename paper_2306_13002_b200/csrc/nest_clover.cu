@@ -34,6 +34,7 @@ void register_clover() {
         fill_march<gen::pdv_predict, double, 0, 64, 1, 64, 1, 4>(e, 0);
         fill_march<gen::pdv_predict, double, 0, 128, 1, 128, 1, 5>(e, 0);
         fill_march<gen::pdv_predict, double, 0, 128, 1, 128, 1, 7>(e, 0);
+        fill_march<gen::pdv_predict, double, 0, 128, 1, 128, 1, 3, 1, 12>(e, 0);   // 12-row chunks
         register_entry(&e);
     }
     {
@@ -47,6 +48,7 @@ void register_clover() {
         fill_march<gen::advec_cell_x, double, 0, 64, 1, 64, 1, 4>(e, 0);
         fill_march<gen::advec_cell_x, double, 0, 128, 1, 128, 1, 5>(e, 0);
         fill_march<gen::advec_cell_x, double, 0, 128, 1, 128, 1, 7>(e, 0);
+        fill_march<gen::advec_cell_x, double, 0, 128, 1, 128, 1, 3, 1, 12>(e, 0);   // 12-row chunks
         register_entry(&e);
     }
 }

@@ -18,6 +18,7 @@ void register_swim() {
         fill_march<gen::calc1, double, 0, 128, 1, 128, 1, 3>(e, 0);
         fill_march<gen::calc1, double, 0, 128, 1, 64, 1, 3>(e, 0);
         fill_march<gen::calc1, double, 0, 64, 1, 64, 1, 4>(e, 0);
+        fill_march<gen::calc1, double, 0, 128, 1, 128, 1, 3, 1, 4>(e, 0);   // 4-row chunks (kchunk sweep)
         register_entry(&e);
     }
     {
