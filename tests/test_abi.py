@@ -114,3 +114,21 @@ def test_native_offset(kid, name, esize, want):
     if want:
         lo = 2 if kid.startswith("wave4") else 1     # the innermost loop's first interior point
         assert ((want + lo) * esize) % 32 == 0
+
+
+@pytest.mark.parametrize("kid", sorted(nests.KERNELS))
+def test_schedule_table(kid):
+    """Slot 0 is the naive skeleton for every nest (the ORIGINAL form's faithful
+    baseline); tiled slots follow, at most kMaxSched = 8, each with a unique
+    name (the tuner reports choices by slot and name)."""
+    names = [n for n in backend.Kernel.lookup(kid).info["schedules"][0] if n]
+    assert names and names[0].startswith("naive")
+    assert 1 < len(names) <= 8
+    assert len(set(names)) == len(names), names
+
+
+def test_two_d_march_chunk_slots_registered():
+    """The k-chunk sweep's extra row-strip slots (profiles/r01_kchunk_sweep_2d.jsonl)."""
+    for kid, rows in [("swim.c:calc1:0", 4), ("clover.c:pdv_predict:1", 12), ("clover.c:advec_cell_x:2", 12)]:
+        names = backend.Kernel.lookup(kid).info["schedules"][0]
+        assert any(n.endswith(f"k-chunk {rows}") for n in names), (kid, names)
