@@ -86,3 +86,36 @@ def run(spec, arrays: Dict[str, np.ndarray], scalars: Dict[str, float], variant:
         fn = getattr(lib(), sym)
         fn.argtypes = [ctypes.c_void_p] * 4
         fn(a, d, iv, dv)
+
+
+_FILL_KIND = {"uniform": 0, "const": 1, "mask": 2, "d3q19": 3}
+
+
+def host_inputs(w, threads: int = 0) -> Dict[str, np.ndarray]:
+    """Reference-layout host inputs of a nests.Workload, filled in place by
+    oracle/fill.c (OpenMP) — bit-identical to nests.make_inputs, without its
+    full-size numpy temporaries.  For bench.py's reference arm."""
+    import os as _os
+    from paper_2306_13002_b200 import nests
+    f = lib().acs_cpu_fill
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
+                  ctypes.c_double, ctypes.c_double, ctypes.c_int64, ctypes.c_int]
+    threads = threads or _os.cpu_count() or 1
+    fdt = np.float32 if w.dtype == "f32" else np.float64
+    out: Dict[str, np.ndarray] = {}
+    for p in w.spec.arrays:
+        shape = w.dims[p.name]
+        fl = w.fills[p.name]
+        dt = np.int32 if p.ctype == "int" else fdt
+        if fl.kind == "copy":
+            out[p.name] = out[fl.src].copy()
+            continue
+        a = np.empty(shape, dtype=dt)
+        code = 2 if dt == np.int32 else (1 if dt == np.float32 else 0)
+        lo = fl.value if fl.kind == "const" else fl.lo
+        if f(a.ctypes.data, a.size, code, _FILL_KIND[fl.kind], nests.SEED_BASE + p.position, lo, fl.hi, fl.p, 0,
+             threads):
+            raise RuntimeError(f"acs_cpu_fill failed for {p.name}")
+        out[p.name] = a
+    return out

@@ -66,3 +66,22 @@ def test_oracle_omp_driver_equals_serial(path):
     oracle_cpu.run(spec, a2, scalars, "accsat", threads=3)
     for k in a1:
         assert np.array_equal(a1[k], a2[k])
+
+
+@pytest.mark.parametrize("kid,size,dtype", [("jacobi7.c:jacobi7:0", (5, 6, 7), "f64"),
+                                            ("d3q19.c:stream_collide:0", (4, 5, 6), "f64"),
+                                            ("wave4.c:wave4:0", (6, 5, 9), "f32"),
+                                            ("swim.c:calc2:1", (9, 11), "f64"),
+                                            ("clover.c:pdv_predict:1", (7, 9), "f64"),
+                                            ("zsolve.c:z_solve_lhs:0", (3, 4, 5), "f64")])
+def test_host_fill_matches_make_inputs(kid, size, dtype):
+    """oracle/fill.c (the reference arm's input generator) is bit-identical to
+    nests.make_inputs for every fill kind."""
+    w = nests.workload(kid, size, dtype=dtype)
+    want = nests.make_inputs(w)
+    got = oracle_cpu.host_inputs(w, threads=3)
+    assert set(got) == set(want)
+    for n in want:
+        assert got[n].dtype == want[n].dtype and got[n].shape == want[n].shape, n
+        u = {8: np.uint64, 4: np.uint32}[want[n].itemsize]
+        assert np.array_equal(got[n].view(u), want[n].view(u)), n
