@@ -1,24 +1,29 @@
 #!/usr/bin/env python3
 """bench.py — B200 loop-nest execution backend benchmark (one JSON line).
 
-Workload (the N=1 line): BASELINE.json configs[1], D3Q19 lattice-Boltzmann
-collide + push-stream, 256^3 fp64 (olbm-like), in the saturated form (the
-reference optimizer's accsat output, frozen in tests/golden/emitted/), one
-step = one stream_collide sweep src -> dst (ping-pong).  The per-kernel table
-(`per_kernel`) covers every BASELINE nest in the original and saturated forms.
+Workload (every N): BASELINE.json configs[4], the seismic wave4 4th-order 3-D
+acoustic wave propagation nest, 1024^3 fp32, in the saturated form, one time
+step per step (3-level buffer rotation up <- u <- un), strong-scaled over N
+z slabs (the scaling case of the metric's "1/2/4/8 GPU").
+N = 1 runs the same slab code with one slab (no neighbours = a plain launch),
+so BENCH N=1 and SCALE N=1 are the same measurement.  `per_kernel` covers
+every BASELINE nest (configs[0]-[3] and zsolve) in the original and
+saturated forms; `--workload d3q19` runs configs[1] (D3Q19 256^3 fp64,
+weak-scaled z slabs for N > 1) as the headline instead.
 
-  value   algorithmic GB/s of the D3Q19 step with inputs resident in HBM
-          (305 B per cell: 19 reads + 19 writes of 8 B + the flag byte,
-          SURVEY.md §8d), whole job over all ranks.  The inputs (5.2 GB) are
-          far larger than the 126 MB L2, so no L2 flush is needed between steps.
-  e2e     the same metric through the public API (backend.eval_region-style
-          path: pinned host buffers in the reference layout -> H2D -> AoS->SoA
-          remap -> kernel -> SoA->AoS -> D2H) with the copies inside the timed
-          region.
+  value   algorithmic GB/s of the step with inputs resident in HBM (16 B per
+          point for wave4: 3 reads + 1 write of 4 B), whole
+          job over all ranks (max-over-ranks step time).  Inputs (17 GB) are
+          far larger than the 126 MB L2: no flush needed between steps.
+  e2e     the same metric through the public host-buffer API: pinned
+          reference-layout host arrays -> H2D -> remap -> kernel -> remap ->
+          D2H, every copy inside the timed region.
 
---impl reference: the reference's own CPU path for the nest — the emitted
-accsat C compiled by gcc -O3 -ffp-contract=off (satcc's wrapper mode,
-proj/tools/satcc_main.cpp:285-360), OpenMP over all host cores.
+--impl reference: the reference's own CPU path for the nest — the reference
+optimizer's emitted accsat C compiled by gcc -O3 -ffp-contract=off (satcc's
+wrapper mode, proj/tools/satcc_main.cpp:285-360), OpenMP over all host
+cores, inputs generated on the host (oracle/fill.c), nothing from this
+repo's GPU library loaded.
 """
 import argparse
 import json
@@ -35,7 +40,12 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 METRIC = "per-kernel GB/s (% B200 HBM roofline), saturated vs original speedup, 1/2/4/8 GPU"
-WORKLOAD_KID = "d3q19.c:stream_collide:0"
+
+WORKLOADS = {
+    # name: (kernel id, dtype, grid per --size default, scaling)
+    "wave4": ("wave4.c:wave4:0", "f32", 1024, "strong"),
+    "d3q19": ("d3q19.c:stream_collide:0", "f64", 256, "weak"),
+}
 
 # per-kernel table: (kernel id, BASELINE size, dtype, sweeps per step)
 TABLE = [
@@ -116,6 +126,24 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def workload_config(workload, size, ws, variant):
+    """The `config` object — identical in both arms (ours and --impl reference)."""
+    kid, dtype, _, scaling = WORKLOADS[workload]
+    if workload == "wave4":
+        grid = [size] * 3
+        name = ("seismic wave4 4th-order 3-D acoustic wave propagation fp32 (BASELINE configs[4]), "
+                "one time step per step, 3-level buffer rotation")
+        bpp = 16
+    else:
+        grid = [size, size, size * ws]
+        name = ("D3Q19 lattice-Boltzmann collide+stream (olbm-like) fp64 (BASELINE configs[1]), "
+                "one sweep per step, src <-> dst")
+        bpp = 305
+    return {"workload": name, "kernel_id": kid, "grid": grid, "form": variant, "dtype": dtype,
+            "bytes_per_point": bpp, "points": int(np.prod(grid)), "scaling": scaling,
+            "l2": "inputs >> 126 MB L2 (no flush needed)"}
+
+
 def dist_setup(args):
     import torch
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -123,8 +151,6 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        if args.impl == "reference":
-            return rank, ws, local, None
         if os.environ.get("ACS_BENCH_SAME_DEVICE"):
             # functional check of the N-rank path on a one-GPU box (numbers meaningless)
             torch.cuda.set_device(0)
@@ -162,7 +188,272 @@ def time_steps(fn, steps, warmup, stream, dist=None):
     return ms
 
 
-def tune_kernel(kid, size, dtype, variant="accsat"):
+def time_reps(fn, reps, warmup, stream):
+    """Per-repetition CUDA-event times (ms) of `fn` on `stream`."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    ev[0].record(stream)
+    for i in range(reps):
+        fn()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    return [ev[i].elapsed_time(ev[i + 1]) for i in range(reps)]
+
+
+def stats(ms):
+    q1, med, q3 = (float(x) for x in np.percentile(ms, [25, 50, 75]))
+    return med, q3 - q1
+
+
+# ---------------------------------------------------------------------------
+# the headline: slab-sharded time steps (N = 1: one slab)
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="wave4", choices=sorted(WORKLOADS))
+    ap.add_argument("--variant", default="accsat")
+    ap.add_argument("--schedule", default="default")
+    ap.add_argument("--size", type=int, default=0, help="interior extent (default: the BASELINE size)")
+    ap.add_argument("--no-table", action="store_true", help="skip the per-kernel table")
+    ap.add_argument("--table-reps", type=int, default=30)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="enqueue every step eagerly (no CUDA graph)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "peer", "nccl"],
+                    help="N>1 halo path: peer memory (CUDA IPC write-through), NCCL P2P, or auto (peer, else NCCL)")
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--e2e-chunks", type=int, default=16)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    args.size = args.size or WORKLOADS[args.workload][2]
+    if isinstance(args.schedule, str) and args.schedule.isdigit():
+        args.schedule = int(args.schedule)     # an explicit registered slot (0 = naive)
+
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    from paper_2306_13002_b200 import shard
+    rank, ws, local, dist = dist_setup(args)
+    peak, peak_kind = load_peaks()
+    kid, dtype, _, scaling = WORKLOADS[args.workload]
+    size = (args.size,) * 3 if args.workload == "wave4" else (args.size * ws, args.size, args.size)
+    sr = shard.SlabRank(kid, size, ws, rank, dtype=dtype, variant=args.variant, schedule=args.schedule)
+    stream = torch.cuda.current_stream()
+    tuned = None
+    if args.schedule == "default" and args.variant != "original":
+        tuned, tuned_ms = sr.k.tune(sr.buf, dict(sr.w.scalars), args.variant, reps=5)   # untimed autotune
+        sr.schedule = tuned
+        sr.refill()
+    torch.cuda.synchronize()
+    exchange = "none"
+    if ws > 1:
+        exchange = connect_ranks(args, sr, dist, rank, ws)
+        if exchange is None:
+            return 3
+    graph = False
+    if sr.mode != "p2p" and not args.no_graph:
+        sr.capture(stream)
+        graph = True
+    if dist:
+        dist.barrier()
+    per_step = {"none": 1, "peer": 3, "p2p": None}[sr.mode]
+    if per_step is None:
+        per_step = 1 + (rank > 0) + (rank < ws - 1)       # interior + boundary slabs
+    for _ in range(args.warmup):
+        sr.step(stream=stream)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = time_steps(lambda: sr.step(stream=stream), args.steps, 0, stream, dist)
+    local_bytes = sr.w.algorithmic_bytes
+    total_bytes = sr.gw.algorithmic_bytes
+    value = total_bytes / (ms * 1e-3) / 1e9
+    slot = sr.schedule if isinstance(sr.schedule, int) else None
+    sched_name = sr.k.info["schedules"][1 if dtype == "f32" else 0][slot] if slot is not None else str(sr.schedule)
+    out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": scaling,
+           "vs_baseline": None, "dtype": dtype,
+           "data": "synthetic (seeded SplitMix64, SURVEY.md §8d distributions; generated in HBM)",
+           "config": workload_config(args.workload, args.size, ws, args.variant),
+           "gpu_launches": per_step * args.steps,
+           "execution": {"parallelism": f"z-slab sharding x{ws}" + ("" if ws == 1 else f", exchange: {exchange}"),
+                         "slab_planes": sr.plan.owned(rank)[1] - sr.plan.owned(rank)[0],
+                         "step": ("one CUDA graph replay per step: " +
+                                  ("wait_ctr -> sharded launch (write-through) -> signal_ctr" if sr.mode == "peer"
+                                   else "one launch")) if graph else
+                                 ("boundary planes -> NCCL P2P halo exchange on a comm stream | interior planes"
+                                  if sr.mode == "p2p" else "eager launch"),
+                         "schedule": sched_name, "tuned_slot": tuned,
+                         "layout": "row-major, 16-element padded pitch, sector-aligned rows"
+                                   if args.workload == "wave4" else "q-major SoA"}}
+    achieved = local_bytes / (ms * 1e-3) / 1e9
+    kname = "wave4_f32" if args.workload == "wave4" else "stream_collide"
+    out["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                       "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
+                       "traffic": load_traffic(kname),
+                       "kernel": f"{kname} {args.variant}: {sched_name}",
+                       "per_unit": f"{sr.w.bytes_per_point} B/point x {sr.w.points} points per launch "
+                                   "(rank 0's slab), over the step's CUDA-event time"}
+    out["clocks"] = clk.summary()
+    if not args.no_e2e:
+        if ws == 1:
+            sr.close()
+            del sr.buf
+            torch.cuda.empty_cache()
+            out["e2e"] = e2e_host_runner(args, sr.gw, sr.k, dist)
+        else:
+            out["e2e"] = e2e_sharded(args, sr, dist, ws)
+    sr.close()
+    del sr
+    torch.cuda.empty_cache()
+    if not args.no_table and ws == 1:
+        out["per_kernel"] = per_kernel_table(peak, args.table_reps)
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(args)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out))
+    return 0
+
+
+def connect_ranks(args, sr, dist, rank, ws):
+    """Wires the slab neighbours: CUDA-IPC peer memory (write-through from the
+    kernel), else NCCL P2P halo exchange.  Never falls back to replicas:
+    returns None (the bench then exits non-zero) when neither works."""
+    err = None
+    if args.exchange in ("auto", "peer"):
+        exp = [None] * ws
+        dist.all_gather_object(exp, sr.export())
+        try:
+            sr.connect_ipc(exp[rank - 1] if rank > 0 else None, exp[rank + 1] if rank < ws - 1 else None)
+        except Exception as e:     # no peer access between these GPUs
+            err = str(e)[:200]
+        errs = [None] * ws
+        dist.all_gather_object(errs, err)
+        err = next((e for e in errs if e), None)
+        if err is None:
+            return "peer memory (CUDA IPC over NVLink), in-kernel write-through + device flags"
+        sr.close()
+        sr.lo_ptr, sr.hi_ptr, sr.lo_flag, sr.hi_flag = {}, {}, None, None
+        print(f"[bench] rank {rank}: peer memory unavailable ({err})", file=sys.stderr)
+        if args.exchange == "peer":
+            return None
+    try:
+        sr.connect_p2p(dist)
+    except NotImplementedError as e:
+        print(f"[bench] rank {rank}: {e}", file=sys.stderr)
+        return None
+    return "NCCL P2P (torch.distributed batch_isend_irecv) overlapped with interior planes" + \
+        (f"; peer memory unavailable: {err}" if err else "")
+
+
+def e2e_sharded(args, sr, dist, ws):
+    """Per rank per step: the owned planes of every input array from pinned
+    reference-layout host memory -> device staging -> native remap, queued
+    AFTER the step's wait for the neighbours (their write-through into this
+    rank's halos / push targets cannot race the upload); the sharded step;
+    the owned planes of the produced array -> staging -> D2H."""
+    import torch
+    from paper_2306_13002_b200 import backend, nests
+    stream = torch.cuda.current_stream()
+    names = sr.names
+    lo, hi = sr.plan.local_range(sr.rank)
+    ins = [n for n in names if n in sr.w.read_arrays and len(sr.w.dims[n]) >= 2]
+    host = {n: torch.empty(tuple(sr.buf[n].shape), dtype=sr.buf[n].dtype, pin_memory=True) for n in names}
+    rm = {n: torch.empty(tuple(sr.buf[n].shape), dtype=sr.buf[n].dtype, device="cuda") for n in names}
+    for n in names:
+        backend.copy(rm[n], sr.buf[n])
+        host[n].copy_(rm[n])
+    torch.cuda.synchronize()
+    out_name = sr.w.write_arrays[0]      # the produced array: D3Q19 dst, wave4 un
+    sr.graphs = None                     # eager: the uploads go between wait and launch
+
+    def upload(s, h):
+        roles = nests.role_buffers(sr.nest, names, s)
+        for p in ins:
+            rm[p][lo:hi].copy_(host[p][lo:hi], non_blocking=True)
+            backend.copy(sr.buf[roles[p]][lo:hi], rm[p][lo:hi], stream)
+
+    def step():
+        s = sr.step_no
+        sr.step(stream=stream, before_launch=upload)
+        roles = nests.role_buffers(sr.nest, names, s)
+        backend.copy(rm[out_name][lo:hi], sr.buf[roles[out_name]][lo:hi], stream)
+        host[out_name][lo:hi].copy_(rm[out_name][lo:hi], non_blocking=True)
+
+    steps = max(3, min(args.steps, 10))
+    ms = time_steps(step, steps, 2, stream, dist)
+    h2d = sum(host[n][lo:hi].numel() * host[n].element_size() for n in ins)
+    d2h = host[out_name][lo:hi].numel() * host[out_name].element_size()
+    total = sr.gw.algorithmic_bytes
+    return {"value": round(total / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3), "steps": steps,
+            "path": "per rank: owned planes of the inputs, pinned host (reference layout) -> H2D -> remap -> "
+                    "sharded step -> remap -> D2H of the produced planes"}
+
+
+def load_traffic(kernel_name):
+    """dram bytes per launch from the committed ncu summary, if present."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel_name)
+    except Exception:
+        return None
+
+
+def e2e_host_runner(args, w, k, dist):
+    """Same metric through the public host-buffer API with every copy inside
+    the timed region: pinned reference-layout host arrays, chunked
+    H2D -> remap -> kernel -> remap -> D2H with the three overlapped on
+    separate streams (paper_2306_13002_b200/pipeline_exec.HostRunner)."""
+    import torch
+    from paper_2306_13002_b200 import nests, pipeline_exec
+    stream = torch.cuda.current_stream()
+    # host inputs in the reference layout (generated on device, copied once, untimed)
+    dev_rm = nests.device_inputs(w, native=False, kernel=k)
+    host = {n: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for n, t in dev_rm.items()}
+    for n, t in dev_rm.items():
+        host[n].copy_(t)
+    del dev_rm
+    torch.cuda.synchronize()
+    runner = pipeline_exec.HostRunner(k, host, w.spec.range_params, chunks=args.e2e_chunks)
+    sc = dict(w.scalars)
+    step = lambda: runner.run(sc, args.variant, args.schedule)   # noqa: E731
+    graph = None
+    if not args.no_graph:
+        try:
+            graph = runner.capture(sc, args.variant, args.schedule)
+            step = graph.replay   # same copies and launches, no host work per chunk
+        except Exception as e:    # report, never hide: fall back to eager enqueue
+            print(f"[bench] e2e graph capture failed, eager: {e}", file=sys.stderr)
+    steps = max(3, min(args.steps, 10))
+    ms = time_steps(step, steps, 2, stream, dist)
+    h2d, d2h = runner.bytes_per_call()
+    res = {"value": round(w.algorithmic_bytes / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3),
+           "steps": steps, "chunks": args.e2e_chunks,
+           "path": "pinned host (reference layout) -> chunked H2D | acs_copy remap + acs_launch | remap + D2H, "
+                   "three overlapped streams (pipeline_exec.HostRunner)"
+                   + (", captured once as a CUDA graph and replayed" if graph is not None else ", eager enqueue")}
+    del runner, host
+    torch.cuda.empty_cache()
+    return res
+
+
+# ---------------------------------------------------------------------------
+# per-kernel table: every nest, original vs saturated, naive vs tuned skeleton
+
+def tune_kernel(kid, size, dtype, variant):
     """acs_tune on the BASELINE-size arrays (untimed); returns (slot, name, {slot: ms})."""
     import torch
     from paper_2306_13002_b200 import backend, nests
@@ -176,34 +467,31 @@ def tune_kernel(kid, size, dtype, variant="accsat"):
     return best, name, ms
 
 
-def bench_kernel(kid, size, dtype, sweeps, variant, schedule, reps=5, warmup=3):
-    """Device-resident GB/s of one nest at its BASELINE size (ping-pong
-    where the nest has a read/write pair)."""
+def bench_kernel(kid, size, dtype, sweeps, variant, schedule, reps, warmup=3):
+    """Device-resident GB/s of one nest at its BASELINE size (ping-pong / 3-level
+    rotation where the nest has one); median and IQR over `reps` steps."""
     import torch
     from paper_2306_13002_b200 import backend, nests
     w = nests.workload(kid, size, dtype=dtype)
     k = backend.Kernel.lookup(kid)
     arrs = nests.device_inputs(w, native=True, kernel=k)
     sc = dict(w.scalars)
-    pair = {"jacobi7": ("A0", "Anext"), "d3q19": ("src", "dst")}.get(w.spec.nest)
+    names = list(arrs)
     stream = torch.cuda.current_stream()
     state = {"t": 0}
+    period = nests.rotation_period(w.spec.nest)
+
+    def launch(t, st):
+        roles = nests.role_buffers(w.spec.nest, names, t)
+        k.launch({p: arrs[b] for p, b in roles.items()}, sc, variant, schedule, st)
 
     def step():
         for _ in range(sweeps):
-            a = dict(arrs)
-            t = state["t"]
-            if pair and t % 2 == 1:
-                a[pair[0]], a[pair[1]] = arrs[pair[1]], arrs[pair[0]]
-            if w.spec.nest == "wave4":   # 3-level rotation up <- u <- un
-                rot = [arrs["up"], arrs["u"], arrs["un"]]
-                r = t % 3
-                a["up"], a["u"], a["un"] = rot[r], rot[(r + 1) % 3], rot[(r + 2) % 3]
-            k.launch(a, sc, variant, schedule, stream)
-            state["t"] = t + 1
+            launch(state["t"], stream)
+            state["t"] += 1
 
     run = step
-    if sweeps > 1 and sweeps % 2 == 0 and w.spec.nest != "wave4":
+    if sweeps > 1 and sweeps % period == 0:
         # a multi-sweep step (Jacobi: 100 ping-pong sweeps) is one CUDA graph
         # of `sweeps` kernel launches, captured once and replayed: the
         # per-launch host cost leaves the timed region, as in a real time loop
@@ -214,341 +502,62 @@ def bench_kernel(kid, size, dtype, sweeps, variant, schedule, reps=5, warmup=3):
         cs = torch.cuda.Stream()
         cs.wait_stream(stream)
         with torch.cuda.graph(g, stream=cs):
-            for _ in range(sweeps):
-                a = dict(arrs)
-                t = state["t"]
-                if pair and t % 2 == 1:
-                    a[pair[0]], a[pair[1]] = arrs[pair[1]], arrs[pair[0]]
-                k.launch(a, sc, variant, schedule, cs)
-                state["t"] = t + 1
+            for t in range(sweeps):
+                launch(t, cs)
         stream.wait_stream(cs)
         torch.cuda.synchronize()
-        run = lambda: g.replay()  # noqa: E731
-    ms = time_steps(run, reps, warmup, stream)
-    gbs = w.algorithmic_bytes * sweeps / (ms * 1e-3) / 1e9
+        run = g.replay
+    ms = time_reps(run, reps, warmup, stream)
+    med, iqr = stats(ms)
+    gbs = w.algorithmic_bytes * sweeps / (med * 1e-3) / 1e9
     del arrs
     torch.cuda.empty_cache()
-    return ms, gbs, w
+    return {"ms": round(med, 4), "iqr_ms": round(iqr, 4), "gbs": round(gbs, 1)}, w
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--variant", default="accsat")
-    ap.add_argument("--schedule", default="default")
-    ap.add_argument("--size", type=int, default=256)
-    ap.add_argument("--no-table", action="store_true", help="skip the per-kernel table")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-threads", type=int, default=0)
-    ap.add_argument("--e2e-chunks", type=int, default=16)
-    ap.add_argument("--workload", default="d3q19", choices=["d3q19", "wave4"],
-                    help="d3q19: BASELINE configs[1] (N>1: weak-scaled z slabs); wave4: configs[4], "
-                         "1024^3 fp32 strong-scaled over N z slabs (SURVEY.md §8e scaling metric)")
-    ap.add_argument("--e2e-eager", action="store_true", help="enqueue the e2e call eagerly instead of a CUDA graph")
-    ap.add_argument("--e2e-split-d2h", action="store_true", help="two download streams in the e2e pipeline")
-    ap.add_argument("--e2e-ramp", action="store_true", help="smaller first/last chunks in the e2e pipeline (measured: no gain)")
-    args = ap.parse_args()
-    args.warmup = max(3, args.warmup)
-    if isinstance(args.schedule, str) and args.schedule.isdigit():
-        args.schedule = int(args.schedule)     # an explicit registered slot (0 = naive)
-
-    if args.impl == "reference":
-        return reference_arm(args)
-
-    import torch
-    from paper_2306_13002_b200 import backend, nests
-    rank, ws, local, dist = dist_setup(args)
-    peak, peak_kind = load_peaks()
-    if args.workload == "wave4":
-        return main_sharded(args, rank, ws, local, dist, peak, peak_kind)
-    if ws > 1:
-        return main_sharded(args, rank, ws, local, dist, peak, peak_kind)
-    kid = WORKLOAD_KID
-    w = nests.workload(kid, args.size)
-    k = backend.Kernel.lookup(kid)
-    stream = torch.cuda.current_stream()
-    arrs = nests.device_inputs(w, native=True, kernel=k)
-    sc = dict(w.scalars)
-    tuned_slot, tuned_ms = (None, {})
-    if args.schedule == "default" and args.variant != "original":
-        tuned_slot, tuned_ms = k.tune(arrs, sc, args.variant, reps=5)   # untimed autotune
-        arrs = nests.device_inputs(w, native=True, kernel=k)            # fresh inputs
-    flip = {"f": False}
-    launches = {"n": 0}
-
-    def step():
-        a = dict(arrs)
-        if flip["f"]:
-            a["src"], a["dst"] = arrs["dst"], arrs["src"]
-        k.launch(a, sc, args.variant, args.schedule, stream)
-        flip["f"] = not flip["f"]
-        launches["n"] += 1
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    launches["n"] = 0
-    with ClockSampler(local) as clk:
-        ms = time_steps(step, args.steps, 0, stream, dist)
-    n_launch = launches["n"]
-    per_rank_bytes = w.algorithmic_bytes
-    value = ws * per_rank_bytes / (ms * 1e-3) / 1e9
-    achieved = per_rank_bytes / (ms * 1e-3) / 1e9
-
-    out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (seeded SplitMix64, SURVEY.md §8d distributions; generated in HBM)",
-           "config": {"workload": "D3Q19 lattice-Boltzmann collide+stream (olbm-like) fp64, one sweep per step",
-                      "grid": [args.size] * 3, "form": args.variant, "schedule": args.schedule,
-                      "layout": "q-major SoA in HBM", "l2": "inputs 5.2 GB >> 126 MB L2 (no flush needed)",
-                      "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
-                      "bytes_per_point": w.bytes_per_point, "points": w.points},
-           "gpu_launches": n_launch}
-    out["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                       "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
-                       "traffic": load_traffic("stream_collide"),
-                       "kernel": f"stream_collide {args.variant}: " + (
-                           k.info["schedules"][0][tuned_slot] if tuned_slot is not None
-                           else (k.info["schedules"][0][args.schedule] if isinstance(args.schedule, int)
-                                 else args.schedule))}
-    out["config"]["tuned"] = {"slot": tuned_slot, "ms_per_slot": {str(s): round(v, 4) for s, v in tuned_ms.items()}}
-    out["clocks"] = clk.summary()
-
-    del arrs
-    torch.cuda.empty_cache()
-    if not args.no_e2e:
-        out["e2e"] = e2e_d3q19(args, w, k, dist)
-    if not args.no_table and ws == 1:
-        out["per_kernel"] = per_kernel_table(peak)
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(w, args)
-    if dist:
-        dist.destroy_process_group()
-    if rank == 0:
-        print(json.dumps(out))
-
-
-def main_sharded(args, rank, ws, local, dist, peak, peak_kind):
-    """N GPUs.  d3q19: the domain is slab-sharded along z, 256 planes per rank
-    (weak scaling: global grid 256 x 256 x 256N); the pushes that cross a slab
-    face are written straight into the neighbour's distribution array.
-    wave4 (--workload wave4, any N): the 1024^3 fp32 grid split into N z
-    slabs (strong scaling); the new boundary planes of `un` are written into
-    the neighbours' halos.  Both over NVLink (CUDA IPC peer memory, from
-    inside the kernel), steps ordered by device-side flags."""
-    import torch
-    from paper_2306_13002_b200 import backend, nests, shard
-    wave = args.workload == "wave4"
-    kid = "wave4.c:wave4:0" if wave else WORKLOAD_KID
-    gsize = 1024 if args.size == 256 and wave else args.size
-    size = (gsize, gsize, gsize) if wave else (args.size * ws, args.size, args.size)
-    sr = shard.SlabRank(kid, size, ws, rank, dtype="f32" if wave else "f64", variant=args.variant,
-                        schedule=args.schedule)
-    stream = torch.cuda.current_stream()
-    tuned = None
-    if args.schedule == "default" and args.variant != "original":
-        tuned, _ = sr.k.tune(sr.buf, dict(sr.w.scalars), args.variant, reps=5)   # untimed
-        sr.schedule = tuned
-        sr.refill()
-    torch.cuda.synchronize()
-    peer_error = None
-    if ws > 1:
-        exp = [None] * ws
-        dist.all_gather_object(exp, sr.export())
-        try:
-            sr.connect_ipc(exp[rank - 1] if rank > 0 else None, exp[rank + 1] if rank < ws - 1 else None)
-        except Exception as e:     # no peer access between these GPUs
-            peer_error = str(e)[:200]
-        errs = [None] * ws
-        dist.all_gather_object(errs, peer_error)
-        if any(errs):
-            # every rank falls back together: slabs without neighbours (no
-            # halo exchange) — reported as such, never as the sharded number
-            sr.close()
-            sr.lo_ptr, sr.hi_ptr, sr.lo_flag, sr.hi_flag = {}, {}, None, None
-            peer_error = next(e for e in errs if e)
-            print(f"[bench] rank {rank}: peer memory unavailable ({peer_error}); running slabs as replicas",
-                  file=sys.stderr)
-        dist.barrier()
-    launches = {"n": 0}
-
-    def step():
-        sr.step(stream=stream)
-        launches["n"] += 1 + (1 if sr.step_no > 1 and (sr.lo_ptr or sr.hi_ptr) else 0) + (1 if sr.lo_flag or sr.hi_flag else 0)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    launches["n"] = 0
-    with ClockSampler(local) as clk:
-        ms = time_steps(step, args.steps, 0, stream, dist)
-    local_bytes = sr.w.algorithmic_bytes
-    total_bytes = sr.gw.algorithmic_bytes if wave else ws * local_bytes
-    value = total_bytes / (ms * 1e-3) / 1e9
-    if wave:
-        cfg = {"workload": "seismic wave4 4th-order 3-D wave propagation fp32, one step per step (3-level rotation)",
-               "grid": [gsize] * 3, "per_rank_planes": sr.plan.owned(rank)[1] - sr.plan.owned(rank)[0],
-               "form": args.variant, "schedule": args.schedule, "tuned_slot": tuned,
-               "parallelism": f"z-slab sharding x{ws} (strong scaling), fused peer-memory halo write-through + "
-                              "device flags",
-               "layout": "row-major, padded pitch", "l2": "inputs >> L2 (no flush needed)",
-               "bytes_per_point": sr.w.bytes_per_point}
-    else:
-        cfg = {"workload": "D3Q19 lattice-Boltzmann collide+stream (olbm-like) fp64, one sweep per step",
-               "grid": [args.size, args.size, args.size * ws], "per_rank_grid": [args.size] * 3,
-               "form": args.variant, "schedule": args.schedule, "tuned_slot": tuned,
-               "parallelism": f"z-slab sharding x{ws}, fused peer-memory push exchange + device flags",
-               "layout": "q-major SoA in HBM", "l2": "inputs >> L2 (no flush needed)",
-               "bytes_per_point": sr.w.bytes_per_point}
-    out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-           "scaling": "strong" if wave else "weak", "vs_baseline": None, "dtype": "f32" if wave else "f64",
-           "data": "synthetic (seeded SplitMix64, SURVEY.md §8d distributions; generated in HBM)",
-           "config": cfg, "gpu_launches": launches["n"]}
-    if peer_error:
-        out["config"]["parallelism"] = f"replicas x{ws}: peer memory unavailable, no halo exchange ({peer_error})"
-    achieved = local_bytes / (ms * 1e-3) / 1e9
-    out["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                       "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
-                       "traffic": load_traffic("wave4_f32" if wave else "stream_collide"),
-                       "kernel": ("wave4_f32 " if wave else "stream_collide ") + args.variant + " (sharded, per rank)"}
-    out["clocks"] = clk.summary()
-    if not args.no_e2e:
-        if ws == 1:
-            # one slab: the overlapped host-buffer pipeline (as for the D3Q19 line)
-            sr.close()
-            del sr.buf
-            torch.cuda.empty_cache()
-            out["e2e"] = e2e_d3q19(args, sr.gw, sr.k, dist)
-        else:
-            out["e2e"] = e2e_sharded(args, sr, dist, ws)
-    sr.close()
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
-    if rank == 0:
-        print(json.dumps(out))
-    return 0
-
-
-def e2e_sharded(args, sr, dist, ws):
-    """Per rank per step: its slab's reference-layout host buffers -> device ->
-    remap -> sharded step (with the peer exchange) -> remap -> host."""
-    import torch
-    from paper_2306_13002_b200 import backend, shard
-    stream = torch.cuda.current_stream()
-    names = [a.name for a in sr.w.spec.arrays]
-    host = {n: torch.empty(tuple(sr.buf[n].shape), dtype=sr.buf[n].dtype, pin_memory=True) for n in names}
-    rm = {n: torch.empty(tuple(sr.buf[n].shape), dtype=sr.buf[n].dtype, device="cuda") for n in names}
-    for n in names:
-        backend.copy(rm[n], sr.buf[n])
-        host[n].copy_(rm[n])
-    torch.cuda.synchronize()
-
-    out_name = sr.w.write_arrays[0]      # the produced array: D3Q19 dst, wave4 un
-
-    def step():
-        roles = shard.role_buffers(sr.nest, names, sr.step_no)
-        for p in names:
-            rm[p].copy_(host[p], non_blocking=True)
-            backend.copy(sr.buf[roles[p]], rm[p], stream)
-        sr.step(stream=stream)
-        backend.copy(rm[out_name], sr.buf[roles[out_name]], stream)
-        host[out_name].copy_(rm[out_name], non_blocking=True)
-
-    steps = max(3, min(args.steps, 10))
-    ms = time_steps(step, steps, 2, stream, dist)
-    h2d = sum(host[n].numel() * host[n].element_size() for n in names)
-    d2h = host[out_name].numel() * host[out_name].element_size()
-    total = sr.gw.algorithmic_bytes if args.workload == "wave4" else ws * sr.w.algorithmic_bytes
-    return {"value": round(total / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3), "steps": steps,
-            "path": "per rank: pinned host slab (reference AoS) -> H2D -> remap -> sharded acs_launch -> remap -> D2H"}
-
-
-def load_traffic(kernel_name):
-    """dram bytes per launch from the committed ncu summary, if present."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
-    try:
-        with open(path) as f:
-            return json.load(f).get(kernel_name)
-    except Exception:
-        return None
-
-
-def e2e_d3q19(args, w, k, dist):
-    """Same metric through the public host-buffer API with every copy inside
-    the timed region: pinned reference-layout (AoS) host arrays, chunked
-    H2D -> remap -> kernel -> remap -> D2H with the three overlapped on
-    separate streams (paper_2306_13002_b200/pipeline_exec.HostRunner)."""
-    import torch
-    from paper_2306_13002_b200 import nests, pipeline_exec
-    stream = torch.cuda.current_stream()
-    # host inputs in the reference layout (generated on device, copied once, untimed)
-    dev_rm = nests.device_inputs(w, native=False, kernel=k)
-    host = {n: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for n, t in dev_rm.items()}
-    for n, t in dev_rm.items():
-        host[n].copy_(t)
-    del dev_rm
-    torch.cuda.synchronize()
-    runner = pipeline_exec.HostRunner(k, host, w.spec.range_params, chunks=args.e2e_chunks, ramp=args.e2e_ramp)
-    runner.split_d2h = args.e2e_split_d2h
-    sc = dict(w.scalars)
-
-    def step():
-        runner.run(sc, args.variant, args.schedule)
-
-    graph = None
-    if not args.e2e_eager:
-        try:
-            graph = runner.capture(sc, args.variant, args.schedule)
-            step = graph.replay   # noqa: F811 — same copies and launches, no host work per chunk
-        except Exception as e:    # report, never hide: fall back to eager enqueue
-            print(f"[bench] e2e graph capture failed, eager: {e}", file=sys.stderr)
-    steps = max(3, min(args.steps, 10))
-    ms = time_steps(step, steps, 2, stream, dist)
-    ws = dist.get_world_size() if dist else 1
-    h2d, d2h = runner.bytes_per_call()
-    res = {"value": round(ws * w.algorithmic_bytes / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
-           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3),
-           "steps": steps, "chunks": args.e2e_chunks,
-           "path": "pinned host (reference AoS layout) -> chunked H2D | acs_copy remap + acs_launch | remap + D2H, "
-                   "three overlapped streams (pipeline_exec.HostRunner)"
-                   + (", captured once as a CUDA graph and replayed" if graph is not None else ", eager enqueue")}
-    del runner, host
-    torch.cuda.empty_cache()
-    return res
-
-
-def per_kernel_table(peak):
+def per_kernel_table(peak, reps):
     rows = {}
     for kid, size, dtype, sweeps in TABLE:
         fn = kid.split(":")[1]
-        row = {"size": size, "dtype": dtype, "sweeps_per_step": sweeps}
+        row = {"size": size, "dtype": dtype, "sweeps_per_step": sweeps, "reps": reps,
+               "timing": f"median and IQR of {reps} CUDA-event-timed steps"}
         if sweeps > 1:
             row["launch"] = f"CUDA graph of {sweeps} kernel launches per step (every form alike)"
-        try:
-            slot, name, tms = tune_kernel(kid, size, dtype, "accsat")
-            row["tuned"] = {"slot": slot, "schedule": name, "ms_per_slot": {str(s): round(v, 4) for s, v in tms.items()}}
-        except Exception as e:
-            row["tuned"] = {"error": str(e)[:200]}
-        for variant, sched in (("original", "naive"), ("original-nvcc", "naive"), ("accsat", "naive"),
-                               ("accsat", "default")):
+        slots = {}
+        for variant in ("accsat", "original"):
             try:
-                ms, gbs, w = bench_kernel(kid, size, dtype, sweeps, variant, sched, reps=5)
-                row[f"{variant}/{sched}"] = {"ms": round(ms, 4), "gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}
+                slot, name, tms = tune_kernel(kid, size, dtype, variant)
+                slots[variant] = slot
+                row[f"tuned_{variant}"] = {"slot": slot, "schedule": name,
+                                           "ms_per_slot": {str(s): round(v, 4) for s, v in tms.items()}}
+            except Exception as e:
+                row[f"tuned_{variant}"] = {"error": str(e)[:200]}
+        w = None
+        for variant, sched, key in (("original", "naive", "original/naive"),
+                                    ("original", slots.get("original"), "original/tuned"),
+                                    ("original-nvcc", "naive", "original-nvcc/naive"),
+                                    ("accsat", "naive", "accsat/naive"),
+                                    ("accsat", slots.get("accsat"), "accsat/tuned")):
+            if sched is None:
+                continue
+            try:
+                r, w = bench_kernel(kid, size, dtype, sweeps, variant, sched, reps)
+                r["frac"] = round(r["gbs"] / peak, 4)
+                row[key] = r
             except Exception as e:  # report, never hide
-                row[f"{variant}/{sched}"] = {"error": str(e)[:200]}
+                row[key] = {"error": str(e)[:200]}
         try:
-            row["sat_vs_orig_speedup"] = round(row["accsat/default"]["gbs"] / row["original/naive"]["gbs"], 3)
-            row["sat_vs_nvcc_default_speedup"] = round(row["accsat/default"]["gbs"] / row["original-nvcc/naive"]["gbs"], 3)
+            def ratio(a, b):
+                A, B = row[a], row[b]
+                band = A["iqr_ms"] / A["ms"] + B["iqr_ms"] / B["ms"]
+                return {"ratio": round(B["ms"] / A["ms"], 3), "noise_band": round(band, 4),
+                        "not_slower": B["ms"] / A["ms"] >= 1 - band}
+            # best vs best: each form on the skeleton the tuner picked for it
+            row["sat_vs_orig_best"] = ratio("accsat/tuned", "original/tuned")
             # the saturation effect alone: both forms in the same (naive) skeleton
-            row["sat_vs_orig_same_skeleton"] = round(row["accsat/naive"]["gbs"] / row["original/naive"]["gbs"], 3)
+            row["sat_vs_orig_same_skeleton"] = ratio("accsat/naive", "original/naive")
+            row["sat_vs_orig_faithful"] = round(row["original/naive"]["ms"] / row["accsat/tuned"]["ms"], 3)
+            row["sat_vs_nvcc_default"] = round(row["original-nvcc/naive"]["ms"] / row["accsat/tuned"]["ms"], 3)
             row["bytes_per_point"] = w.bytes_per_point
         except Exception:
             pass
@@ -556,55 +565,71 @@ def per_kernel_table(peak):
     return rows
 
 
+# ---------------------------------------------------------------------------
+# CPU: the reference's own path (reported baseline, and the reference arm)
+
 def cpu_threads(args):
     return args.cpu_threads or os.cpu_count() or 1
 
 
-def run_cpu_steps(w, variant, steps, threads, arrays=None):
+def mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    return 0
+
+
+def cpu_workload(args):
+    """The workload the CPU runs: the full configured grid when the host has
+    the memory for it (wave4 1024^3 fp32: 17.4 GB), else a 512^3 sample."""
+    from paper_2306_13002_b200 import nests
+    kid, dtype, _, _ = WORKLOADS[args.workload]
+    n = args.size
+    w = nests.workload(kid, n, dtype=dtype)
+    need = sum(int(np.prod(d)) for d in w.dims.values()) * (4 if dtype == "f32" else 8)
+    if mem_available() < 2 * need + (8 << 30):
+        n = min(args.size, 512)
+        w = nests.workload(kid, n, dtype=dtype)
+    return w, n
+
+
+def run_cpu_steps(w, variant, steps, threads, arrays):
     """Timed steps of the reference's CPU path, buffers rotating like the GPU
     steps (D3Q19 src <-> dst, wave4 up <- u <- un)."""
     import cpu as oracle_cpu
-    from paper_2306_13002_b200 import shard
-    if arrays is None:
-        arrays = host_inputs_via_gpu(w)
+    from paper_2306_13002_b200 import nests
     names = list(arrays)
     ts = []
     for s in range(steps):
-        roles = shard.role_buffers(w.spec.nest, names, s)
+        roles = nests.role_buffers(w.spec.nest, names, s)
         a = {p: arrays[roles[p]] for p in names}
         t0 = time.perf_counter()
         oracle_cpu.run(w.spec, a, w.scalars, variant, threads=threads, f32=w.dtype == "f32")
         ts.append(time.perf_counter() - t0)
-    return ts, arrays
+    return ts
 
 
-def host_inputs_via_gpu(w):
-    """Reference-layout host inputs: generated on the device when a GPU is
-    present (fast), else with numpy (identical values)."""
-    from paper_2306_13002_b200 import nests
-    try:
-        import torch
-        if torch.cuda.is_available():
-            dev = nests.device_inputs(w, native=False)
-            out = {n: t.cpu().numpy() for n, t in dev.items()}
-            del dev
-            torch.cuda.empty_cache()
-            return out
-    except Exception:
-        pass
-    return nests.make_inputs(w)
+def cpu_sample_desc(n, steps):
+    return f"{steps} steps of the {n}^3 grid"
 
 
-def cpu_baseline(w, args):
+def cpu_baseline(args):
+    import cpu as oracle_cpu
+    w, n = cpu_workload(args)
     threads = cpu_threads(args)
-    ts, arrays = run_cpu_steps(w, "accsat", 3, threads)
+    arrays = oracle_cpu.host_inputs(w, threads)
+    run_cpu_steps(w, args.variant, 1, threads, arrays)            # first touch
+    ts = run_cpu_steps(w, args.variant, 3, threads, arrays)
     t = float(np.median(ts))
-    t1, _ = run_cpu_steps(w, "accsat", 1, 1, arrays)      # one core, one sweep (SURVEY §8d)
+    t1 = run_cpu_steps(w, args.variant, 1, 1, arrays)            # one core, one step (SURVEY §8d)
     return {"value": round(w.algorithmic_bytes / t / 1e9, 3), "unit": "GB/s", "cores": threads,
-            "value_1core": round(w.algorithmic_bytes / t1[0] / 1e9, 3),
-            "kind": "reference",
-            "sample": f"3 full {w.dims['flags']} D3Q19 sweeps of the reference-emitted accsat C "
-                      f"(gcc -O3 -ffp-contract=off, OpenMP over z), median",
+            "value_1core": round(w.algorithmic_bytes / t1[0] / 1e9, 3), "kind": "reference",
+            "sample": f"{cpu_sample_desc(n, 3)} (median) of the reference-emitted {args.variant} C "
+                      "(gcc -O3 -ffp-contract=off, OpenMP over the outermost loop); value_1core: one step, one thread",
             "cpu": cpu_model()}
 
 
@@ -620,36 +645,32 @@ def cpu_model():
 
 
 def reference_arm(args):
+    """The reference's CPU path on this box's host cores, same metric / config
+    / steps / warm-up as our arm.  Rank 0 alone runs it under torchrun."""
     rank = int(os.environ.get("RANK", "0"))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    from paper_2306_13002_b200 import nests
-    wave = args.workload == "wave4"
-    # wave4: a bounded 512^3 sample of the 1024^3 workload (4 x 0.54 GB host arrays)
-    w = nests.workload("wave4.c:wave4:0", 512 if args.size == 256 else min(args.size, 512), dtype="f32") if wave \
-        else nests.workload(WORKLOAD_KID, args.size)
+    import cpu as oracle_cpu
+    w, n = cpu_workload(args)
     threads = cpu_threads(args)
-    arrays = host_inputs_via_gpu(w)
-    run_cpu_steps(w, args.variant, 1, threads, arrays)       # warm-up (first touch)
-    steps = max(1, min(args.steps, 10))
-    ts, _ = run_cpu_steps(w, args.variant, steps, threads, arrays)
+    arrays = oracle_cpu.host_inputs(w, threads)                  # host generator: no GPU library
+    run_cpu_steps(w, args.variant, args.warmup, threads, arrays)
+    ts = run_cpu_steps(w, args.variant, args.steps, threads, arrays)
     t = sum(ts) / len(ts)
+    cfg = workload_config(args.workload, args.size, ws, args.variant)
+    total = cfg["points"] * cfg["bytes_per_point"]
+    # GB/s of the steps the CPU ran (a sample when the full grid does not fit)
     v = w.algorithmic_bytes / t / 1e9
-    out = {"metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": steps,
-           "warmup": 1, "ms_per_step": round(t * 1e3, 2), "higher_is_better": True,
-           "scaling": "strong" if wave else "weak",
-           "vs_baseline": None, "dtype": "f32" if wave else "f64", "data": "synthetic (seeded SplitMix64, identical inputs)",
-           "impl": "reference",
-           "config": ({"workload": "seismic wave4 4th-order 3-D wave propagation fp32, one step per step "
-                                   "(3-level rotation)", "grid": [1024] * 3,
-                       "form": args.variant} if wave else
-                      {"workload": "D3Q19 lattice-Boltzmann collide+stream (olbm-like) fp64, one sweep per step",
-                       "grid": [args.size] * 3, "form": args.variant}),
+    out = {"metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(t * 1e3 * total / w.algorithmic_bytes, 2),
+           "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": cfg["dtype"],
+           "data": "synthetic (seeded SplitMix64, SURVEY.md §8d distributions; identical values to our arm)",
+           "impl": "reference", "config": cfg,
            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-                            "sample": (f"{steps} steps on a {round(w.points ** (1 / 3))}^3 sample" if wave
-                                       else f"{steps} full sweeps") +
-                                      f"; reference-emitted {args.variant} C compiled by gcc "
-                                      "-O3 -ffp-contract=off (satcc wrapper mode), OpenMP over z",
+                            "sample": f"{cpu_sample_desc(n, args.steps)} (after {args.warmup} warm-up steps); "
+                                      f"reference-emitted {args.variant} C compiled by gcc -O3 -ffp-contract=off "
+                                      "(satcc wrapper mode), OpenMP over the outermost loop",
                             "cpu": cpu_model()},
            "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))

@@ -46,7 +46,10 @@ typedef enum {
     ACS_E_SHAPE = 3,      /* dims, strides or dtype do not match the kernel's declaration */
     ACS_E_CUDA = 4,       /* CUDA runtime error (message has the CUDA error string) */
     ACS_E_NCCL = 5,       /* peer / collective setup error */
-    ACS_E_BOUNDS = 6      /* iteration space would index outside an array (EvalError analogue) */
+    ACS_E_BOUNDS = 6,     /* iteration space would index outside an array (EvalError analogue) */
+    ACS_E_LAYOUT = 7      /* an explicitly requested schedule slot cannot describe these arrays'
+                             layout (e.g. the TMA needs 16-byte aligned bases and pitches); the
+                             DEFAULT schedule never fails this way (it runs the naive skeleton) */
 } acs_status;
 
 typedef enum { ACS_F64 = 0, ACS_F32 = 1, ACS_I32 = 2, ACS_I64 = 3, ACS_U8 = 4 } acs_dtype;
@@ -213,6 +216,15 @@ acs_status acs_signal(uint64_t* flag_a, uint64_t* flag_b, uint64_t value, void* 
  * (acquire); traps after `timeout_ms` so a lost peer is a loud error, not a hang */
 acs_status acs_wait(const uint64_t* flag_a, const uint64_t* flag_b, uint64_t value, int timeout_ms,
                     void* cuda_stream);
+/* Graph-capturable step ordering: the step number lives in a device counter
+ * (one uint64 per rank, zero before the first step).  acs_wait_ctr blocks the
+ * stream until each non-NULL local flag >= *counter; acs_signal_ctr increments
+ * *counter after all prior work on the stream and release-stores the new value
+ * into each non-NULL (peer) flag.  A (wait_ctr, launch, signal_ctr) sequence
+ * captured once in a CUDA graph is valid for every step. */
+acs_status acs_signal_ctr(uint64_t* flag_a, uint64_t* flag_b, uint64_t* counter, void* cuda_stream);
+acs_status acs_wait_ctr(const uint64_t* flag_a, const uint64_t* flag_b, const uint64_t* counter, int timeout_ms,
+                        void* cuda_stream);
 /* CUDA IPC of a device pointer inside any allocation (base handle + offset) */
 acs_status acs_ipc_export(const void* dptr, void* handle_out /* 64 bytes */, int64_t* offset_out);
 acs_status acs_ipc_import(const void* handle /* 64 bytes */, int64_t offset, void** dptr_out);

@@ -28,7 +28,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libaccsat_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "accsat_b200.h")
 
-ACS_OK, ACS_E_ARG, ACS_E_NO_KERNEL, ACS_E_SHAPE, ACS_E_CUDA, ACS_E_NCCL, ACS_E_BOUNDS = range(7)
+ACS_OK, ACS_E_ARG, ACS_E_NO_KERNEL, ACS_E_SHAPE, ACS_E_CUDA, ACS_E_NCCL, ACS_E_BOUNDS, ACS_E_LAYOUT = range(8)
 F64, F32, I32, I64, U8 = range(5)
 VARIANTS = {"original": 0, "cse": 1, "cse+bulk": 2, "cse+sat": 3, "accsat": 4,
             "original-nvcc": 5}   # measurement baseline: original text, nvcc-default arithmetic
@@ -109,7 +109,7 @@ def _check(status: int, what: str) -> None:
     if status == ACS_OK:
         return
     msg = lib().acs_last_error().decode()
-    if status in (ACS_E_BOUNDS, ACS_E_ARG, ACS_E_SHAPE, ACS_E_NO_KERNEL):
+    if status in (ACS_E_BOUNDS, ACS_E_ARG, ACS_E_SHAPE, ACS_E_NO_KERNEL, ACS_E_LAYOUT):
         raise EvalError(f"{what}: {msg}")
     raise InternalError(f"{what}: {msg}")
 

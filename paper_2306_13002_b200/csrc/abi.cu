@@ -207,6 +207,35 @@ __global__ void wait_kernel(const unsigned long long* a, const unsigned long lon
     __threadfence_system();
 }
 
+// graph-capturable variants: the step value lives in a device counter, so one
+// captured (wait, launch, signal) sequence replays for every step
+__global__ void signal_ctr_kernel(unsigned long long* a, unsigned long long* b, unsigned long long* ctr) {
+    __threadfence_system();
+    const unsigned long long v = *ctr + 1;
+    *ctr = v;
+    if (a) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+    if (b) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(b), "l"(v) : "memory");
+}
+
+__global__ void wait_ctr_kernel(const unsigned long long* a, const unsigned long long* b,
+                                const unsigned long long* ctr, unsigned long long timeout_ns) {
+    const unsigned long long v = *ctr;
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (const unsigned long long* f : {a, b}) {
+        if (!f) continue;
+        for (;;) {
+            unsigned long long x;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(f) : "memory");
+            if (x >= v) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > timeout_ns) __trap();
+            __nanosleep(200);
+        }
+    }
+    __threadfence_system();
+}
+
 extern "C" {
 
 int acs_abi_version(void) { return ACS_ABI_VERSION; }
@@ -419,7 +448,8 @@ static acs_status launch_impl(const acs_kernel* k, acs_variant variant, acs_sche
                   std::to_string(variant) + (prec ? " (fp32)" : ""));
         return ACS_E_NO_KERNEL;
     }
-    LaunchReq r{arrays, n_arrays, scalars, n_scalars, static_cast<cudaStream_t>(cuda_stream), shard};
+    LaunchReq r{arrays, n_arrays, scalars, n_scalars, static_cast<cudaStream_t>(cuda_stream), shard,
+                schedule != ACS_SCHED_DEFAULT && schedule != ACS_SCHED_NAIVE};
     return fn(r);
 }
 
@@ -447,6 +477,28 @@ acs_status acs_wait(const uint64_t* flag_a, const uint64_t* flag_b, uint64_t val
                                                                     (const unsigned long long*)flag_b, value,
                                                                     (unsigned long long)timeout_ms * 1000000ULL);
     return check_launch("acs_wait");
+}
+
+acs_status acs_signal_ctr(uint64_t* flag_a, uint64_t* flag_b, uint64_t* counter, void* cuda_stream) {
+    if (!counter) {
+        set_error("acs_signal_ctr: null counter");
+        return ACS_E_ARG;
+    }
+    signal_ctr_kernel<<<1, 1, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
+        (unsigned long long*)flag_a, (unsigned long long*)flag_b, (unsigned long long*)counter);
+    return check_launch("acs_signal_ctr");
+}
+
+acs_status acs_wait_ctr(const uint64_t* flag_a, const uint64_t* flag_b, const uint64_t* counter, int timeout_ms,
+                        void* cuda_stream) {
+    if (!counter) {
+        set_error("acs_wait_ctr: null counter");
+        return ACS_E_ARG;
+    }
+    wait_ctr_kernel<<<1, 1, 0, static_cast<cudaStream_t>(cuda_stream)>>>(
+        (const unsigned long long*)flag_a, (const unsigned long long*)flag_b, (const unsigned long long*)counter,
+        (unsigned long long)timeout_ms * 1000000ULL);
+    return check_launch("acs_wait_ctr");
 }
 
 acs_status acs_ipc_export(const void* dptr, void* handle_out, int64_t* offset_out) {
@@ -526,7 +578,7 @@ acs_status acs_tune(const acs_kernel* k, acs_variant variant, const acs_array* a
     Entry* e = const_cast<Entry*>(reinterpret_cast<const Entry*>(k));
     const int prec = precision_of(arrays, n_arrays);
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
-    LaunchReq r{arrays, n_arrays, scalars, n_scalars, s};
+    LaunchReq r{arrays, n_arrays, scalars, n_scalars, s, nullptr, true};
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -537,6 +589,7 @@ acs_status acs_tune(const acs_kernel* k, acs_variant variant, const acs_array* a
         LaunchFn fn = e->launch[prec][variant][slot];
         if (!fn) continue;
         acs_status st = fn(r);   // warm-up (and TMA attribute setup)
+        if (st == ACS_E_LAYOUT) continue;   // this skeleton cannot take the layout: not a candidate
         if (st != ACS_OK) {
             cudaEventDestroy(e0);
             cudaEventDestroy(e1);

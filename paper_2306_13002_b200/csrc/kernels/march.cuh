@@ -879,8 +879,14 @@ acs_status launch_march(const LaunchReq& r) {
     TmaMaps<NS> maps;
     std::memset(&maps, 0, sizeof maps);
     if (!encode_maps<NS, T, LAYOUT, TX, TY, RX>(r, maps)) {
-        // layout the TMA cannot describe (unaligned base / pitch): same
+        // layout the TMA cannot describe (unaligned base / pitch): an explicit
+        // slot request fails loudly; the DEFAULT schedule keeps the same
         // numerics through the global-memory skeleton
+        if (r.strict) {
+            set_error(std::string("march skeleton (") + NS::array_names[0] + ", ...) cannot describe this layout with the TMA "
+                      "(16-byte aligned base and pitches needed); use the naive slot or native strides");
+            return ACS_E_LAYOUT;
+        }
         return launch_naive<NS, T, FORM>(r);
     }
     constexpr int D = P::maxspan() + PF;

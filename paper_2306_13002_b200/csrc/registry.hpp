@@ -28,6 +28,7 @@ struct LaunchReq {
     int n_scalars;
     cudaStream_t stream;
     const acs_shard* shard = nullptr;   // slab-sharded launch (acs_launch_sharded)
+    bool strict = false;   // explicit slot: a skeleton that cannot take the layout fails (ACS_E_LAYOUT)
 };
 
 using LaunchFn = acs_status (*)(const LaunchReq&);

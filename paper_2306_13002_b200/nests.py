@@ -312,3 +312,33 @@ def device_inputs(w: Workload, native: bool = True, kernel=None, stream=None):
             backend.fill(t, fl.kind, SEED_BASE + p.position, lo, fl.hi, fl.p, stream)
         out[p.name] = t
     return out
+
+
+# ---------------------------------------------------------------------------
+# Time stepping: the arrays each nest produces and how buffers rotate between
+# steps (Jacobi ping-pong, D3Q19 src <-> dst, wave4 up <- u <- un <- up).
+
+ROTATIONS = {
+    "jacobi7": [("A0", "Anext")],
+    "d3q19": [("src", "dst")],
+    "wave4": [("up", "u", "un")],
+}
+
+
+def role_buffers(nest: str, names, step: int) -> Dict[str, str]:
+    """Parameter name -> physical buffer name at `step` (0-based)."""
+    out = {n: n for n in names}
+    for group in ROTATIONS.get(nest, []):
+        L = len(group)
+        for i, p in enumerate(group):
+            out[p] = group[(i + step) % L]
+    return out
+
+
+def rotation_period(nest: str) -> int:
+    """Steps after which every buffer is back in its starting role."""
+    p = 1
+    for group in ROTATIONS.get(nest, []):
+        p = p * len(group) // np.gcd(p, len(group))
+    return p
+

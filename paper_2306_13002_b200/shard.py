@@ -31,11 +31,8 @@ import numpy as np
 from . import backend, nests
 
 # the arrays each nest produces, and how buffers rotate between steps
-ROTATIONS = {
-    "jacobi7": [("A0", "Anext")],
-    "d3q19": [("src", "dst")],
-    "wave4": [("up", "u", "un")],
-}
+ROTATIONS = nests.ROTATIONS
+role_buffers = nests.role_buffers
 
 
 @dataclass(frozen=True)
@@ -83,6 +80,12 @@ def plan_for(w: nests.Workload, nranks: int) -> SlabPlan:
     dim0 = w.dims[first.name][0]
     reach_lo, reach_hi = glo, dim0 - ghi
     halo = {"jacobi7": 1, "wave4": 2, "d3q19": 0, "swim": 1, "clover": 1}[w.spec.nest]
+    # neighbours exchange only with ranks +-1: every slab must own at least
+    # the planes the next step reads across its face (and one plane at all)
+    need = max(1, halo, reach_lo, reach_hi)
+    if (ghi - glo) // nranks < need:
+        raise ValueError(f"{w.spec.kernel_id}: {ghi - glo} planes over {nranks} ranks leaves slabs thinner than "
+                         f"the {need} planes a neighbour exchange reaches")
     return SlabPlan(glo, ghi, nranks, reach_lo, reach_hi, halo)
 
 
@@ -102,16 +105,6 @@ def local_workload(w: nests.Workload, plan: SlabPlan, rank: int) -> nests.Worklo
                           w.read_arrays, w.write_arrays)
 
 
-def role_buffers(nest: str, names: Sequence[str], step: int) -> Dict[str, str]:
-    """Parameter name -> physical buffer name at `step` (0-based)."""
-    out = {n: n for n in names}
-    for group in ROTATIONS.get(nest, []):
-        L = len(group)
-        for i, p in enumerate(group):
-            out[p] = group[(i + step) % L]
-    return out
-
-
 # ---------------------------------------------------------------------------
 # device side
 
@@ -129,10 +122,10 @@ def _fns():
         L.acs_launch_sharded.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(backend.AcsArray),
                                          ctypes.c_int, ctypes.POINTER(backend.AcsScalar), ctypes.c_int,
                                          ctypes.POINTER(AcsShard), ctypes.c_void_p]
-        L.acs_signal.restype = ctypes.c_int
-        L.acs_signal.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
-        L.acs_wait.restype = ctypes.c_int
-        L.acs_wait.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p]
+        L.acs_signal_ctr.restype = ctypes.c_int
+        L.acs_signal_ctr.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.acs_wait_ctr.restype = ctypes.c_int
+        L.acs_wait_ctr.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
         L.acs_ipc_export.restype = ctypes.c_int
         L.acs_ipc_export.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]
         L.acs_ipc_import.restype = ctypes.c_int
@@ -156,12 +149,70 @@ def ipc_import(handle: bytes, offset: int) -> int:
     return p.value
 
 
+# ---------------------------------------------------------------------------
+# message-passing halo exchange (NCCL over NVLink on GPUs, gloo on CPU tensors)
+
+def plane_view(t, lo: int, hi: int):
+    """Flat view of planes [lo, hi) of `t` (outermost index) covering exactly
+    the elements between the first element of plane lo and the last element
+    of plane hi-1 — padded pitches included, so two buffers with the same
+    strides exchange the same bytes.  Contiguous, as P2P sends need."""
+    torch = backend._torch() if t.is_cuda else __import__("torch")
+    if hi <= lo:
+        return t.new_empty(0)
+    st = t.stride()
+    one = 1 + sum((d - 1) * s for d, s in zip(t.shape[1:], st[1:]))
+    n = (hi - lo - 1) * st[0] + one
+    return torch.as_strided(t, (n,), (1,), t.storage_offset() + lo * st[0])
+
+
+def exchange_ops(rank: int, nranks: int, lo: int, hi: int, halo: int):
+    """The halo exchange of one produced array after a step, in LOCAL plane
+    coordinates of a rank owning [lo, hi): (peer, send planes, recv planes).
+    The lower neighbour gets this rank's first `halo` owned planes and sends
+    its last ones into [lo - halo, lo); symmetrically for the upper one."""
+    out = []
+    if halo <= 0:
+        return out
+    if rank > 0:
+        out.append((rank - 1, (lo, lo + halo), (lo - halo, lo)))
+    if rank < nranks - 1:
+        out.append((rank + 1, (hi - halo, hi), (hi, hi + halo)))
+    return out
+
+
+def halo_exchange(dist, rank: int, nranks: int, t, lo: int, hi: int, halo: int, group=None) -> None:
+    """Sends / receives the boundary planes of `t` with ranks +-1 through
+    torch.distributed P2P (batched: one NCCL group on GPUs).  Enqueued on
+    the CURRENT stream; returns once the receives are ordered before later
+    work on that stream."""
+    ops = []
+    for peer, (slo, shi), (rlo, rhi) in exchange_ops(rank, nranks, lo, hi, halo):
+        ops.append(dist.P2POp(dist.isend, plane_view(t, slo, shi), peer, group))
+        ops.append(dist.P2POp(dist.irecv, plane_view(t, rlo, rhi), peer, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
 class SlabRank:
     """One rank's slab of a nest: local buffers, neighbour pointers, step loop.
 
-    Neighbour buffers are either raw device pointers of another SlabRank in
-    the same process (``connect_local``) or CUDA-IPC imports from other
-    processes (``export`` / ``connect_ipc``)."""
+    Two data paths for the per-step neighbour exchange:
+
+    * **peer memory** (``connect_local`` / ``connect_ipc``): neighbour buffers
+      are raw device pointers (same process, or CUDA-IPC imports over
+      NVLink); the compute kernel writes boundary stores through to them and
+      device flags order the steps (``acs_wait_ctr`` / ``acs_signal_ctr``).
+      A step is (wait, launch, signal) with the step number in a device
+      counter, so it is captured once per rotation phase as a CUDA graph
+      (``capture``) and replayed: no host work per step.
+    * **message passing** (``connect_p2p``, NCCL over NVLink when peer
+      mapping is unavailable): the boundary planes are computed first, handed
+      to a communication stream that exchanges them with ``halo_exchange``
+      while the interior planes compute; the next step waits for the
+      exchange.  Halo-read nests only (jacobi7, wave4): D3Q19's push stream
+      writes into the neighbour's planes and needs peer memory."""
 
     def __init__(self, kernel_id: str, size, nranks: int, rank: int, dtype: str = "f64",
                  variant: str = "accsat", schedule="default"):
@@ -174,22 +225,31 @@ class SlabRank:
         self.w = local_workload(self.gw, self.plan, rank)
         self.variant, self.schedule = variant, schedule
         self.nest = self.gw.spec.nest
+        self.names = [a.name for a in self.w.spec.arrays]
         self.sharded = [g for grp in ROTATIONS[self.nest] for g in grp]
+        self.period = nests.rotation_period(self.nest)
         self.step_no = 0
         self.buf = self._alloc()
-        self.flags = torch.zeros(2, dtype=torch.int64, device="cuda")   # [from lower, from upper]
+        # [from lower, from upper] step flags (neighbours store into them), and
+        # this rank's completed-step counter
+        self.flags = torch.zeros(2, dtype=torch.int64, device="cuda")
+        self.ctr = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.lo_ptr: Dict[str, int] = {}
         self.hi_ptr: Dict[str, int] = {}
         self.lo_flag = self.hi_flag = None    # neighbours' flag words we signal into
         self.lo_origin = self.hi_origin = 0
         self.imported: List[Tuple[int, int]] = []
+        self.mode = "none"                    # none | peer | p2p
+        self.dist = self.group = None
+        self.comm_stream = None
+        self.comm_done = None
+        self.graphs = None
 
     def _alloc(self):
         """Local buffers, filled with the GLOBAL workload's values (flat offset
         of the slab's first plane in the reference layout)."""
         torch = self.torch
         out = {}
-        origin = self.plan.origin(self.rank)
         tdt = torch.float32 if self.w.dtype == "f32" else torch.float64
         # every rank allocates the SAME number of planes (the largest slab), so
         # element strides are identical across ranks — the kernel forwards a
@@ -210,7 +270,10 @@ class SlabRank:
 
     def refill(self, bufs=None) -> None:
         """(Re)writes the slab's initial values: the GLOBAL workload's stream at
-        the slab's reference flat offset, so slabs reproduce the global array."""
+        the slab's reference flat offset, so slabs reproduce the global array.
+        Also restarts the step count (device counter and flags): call it on
+        every rank while no neighbour is stepping, and barrier before the next
+        step."""
         bufs = self.buf if bufs is None else bufs
         origin = self.plan.origin(self.rank)
         for p in self.w.spec.arrays:
@@ -225,6 +288,11 @@ class SlabRank:
                 lo = fl.value if fl.kind == "const" else fl.lo
                 backend.fill(t, fl.kind, nests.SEED_BASE + p.position, lo, fl.hi, fl.p, flat_offset=off)
         self.step_no = 0
+        if hasattr(self, "ctr"):
+            self.torch.cuda.synchronize()
+            self.flags.zero_()
+            self.ctr.zero_()
+            self.torch.cuda.synchronize()
 
     # -- wiring
     def pointers(self) -> Dict[str, int]:
@@ -239,6 +307,8 @@ class SlabRank:
             self.hi_ptr = {n: upper.buf[n].data_ptr() for n in self.sharded}
             self.hi_origin = upper.plan.origin(upper.rank)
             self.hi_flag = upper.flags.data_ptr()            # upper's "from lower" word
+        self.mode = "peer" if (lower is not None or upper is not None) else "none"
+        self.graphs = None
 
     def export(self) -> Dict:
         return {"origin": self.plan.origin(self.rank),
@@ -250,38 +320,53 @@ class SlabRank:
             p = ipc_import(*h)
             self.imported.append((p, h[1]))
             return p
-        if lower is not None:
-            self.lo_ptr = {n: imp(h) for n, h in lower["bufs"].items()}
-            self.lo_origin = lower["origin"]
-            self.lo_flag = imp(lower["flags"]) + 8
-        if upper is not None:
-            self.hi_ptr = {n: imp(h) for n, h in upper["bufs"].items()}
-            self.hi_origin = upper["origin"]
-            self.hi_flag = imp(upper["flags"])
+        try:
+            if lower is not None:
+                self.lo_ptr = {n: imp(h) for n, h in lower["bufs"].items()}
+                self.lo_origin = lower["origin"]
+                self.lo_flag = imp(lower["flags"]) + 8
+            if upper is not None:
+                self.hi_ptr = {n: imp(h) for n, h in upper["bufs"].items()}
+                self.hi_origin = upper["origin"]
+                self.hi_flag = imp(upper["flags"])
+        except Exception:
+            self.close()
+            self.lo_ptr, self.hi_ptr, self.lo_flag, self.hi_flag = {}, {}, None, None
+            raise
+        self.mode = "peer" if (lower is not None or upper is not None) else "none"
+        self.graphs = None
+
+    def connect_p2p(self, dist, group=None) -> None:
+        """Message-passing exchange through torch.distributed (NCCL)."""
+        if self.plan.halo <= 0:
+            raise NotImplementedError(f"{self.k.kernel_id}: the push-stream exchange writes into the neighbour's "
+                                      "planes; it needs peer memory (connect_ipc)")
+        self.mode = "p2p" if self.nranks > 1 else "none"
+        self.dist, self.group = dist, group
+        self.comm_stream = self.torch.cuda.Stream()
+        self.comm_done = self.torch.cuda.Event()
+        self.comm_done.record(self.comm_stream)
+        self.graphs = None
 
     def close(self) -> None:
         for p, off in self.imported:
             _fns().acs_ipc_close(p, off)
         self.imported = []
+        self.graphs = None
 
     # -- stepping
-    def step(self, stream=None, timeout_ms: int = 20000) -> None:
-        """One step: wait for the neighbours' previous step, compute the owned
-        planes with write-through, signal the neighbours."""
+    def _sched(self):
+        return 16 + self.schedule if isinstance(self.schedule, int) else backend.SCHEDULES[self.schedule]
+
+    def _launch(self, s: int, h, scalars=None, write_through: bool = True) -> None:
         L = _fns()
-        h = backend._stream_handle(stream)
-        s = self.step_no
-        if s > 0:
-            backend._check(L.acs_wait(self.flags.data_ptr() if self.lo_ptr else None,
-                                      self.flags.data_ptr() + 8 if self.hi_ptr else None, s, timeout_ms, h),
-                           "acs_wait")
-        roles = role_buffers(self.nest, [a.name for a in self.w.spec.arrays], s)
+        roles = role_buffers(self.nest, self.names, s)
         arrays = {p: self.buf[b] for p, b in roles.items()}
-        descs, sc = self.k._pack(arrays, dict(self.w.scalars))
+        descs, sc = self.k._pack(arrays, dict(scalars or self.w.scalars))
         sd = AcsShard()
         lo, hi = self.plan.owned(self.rank)
         sd.own_lo, sd.own_hi, sd.origin, sd.halo = lo, hi, self.plan.origin(self.rank), self.plan.halo
-        names = [n for n in self.sharded if n in self.w.write_arrays]   # produced arrays only
+        names = [n for n in self.sharded if n in self.w.write_arrays] if write_through else []   # produced arrays
         sd.n_sharded = len(names)
         keep = [n.encode() for n in names]
         for i, n in enumerate(names):
@@ -289,17 +374,94 @@ class SlabRank:
             sd.lo_data[i] = self.lo_ptr.get(roles[n]) if self.lo_ptr else None
             sd.hi_data[i] = self.hi_ptr.get(roles[n]) if self.hi_ptr else None
         sd.lo_origin, sd.hi_origin = self.lo_origin, self.hi_origin
-        sched = 16 + self.schedule if isinstance(self.schedule, int) else backend.SCHEDULES[self.schedule]
-        backend._check(L.acs_launch_sharded(self.k.handle, backend.VARIANTS[self.variant], sched, descs, len(arrays),
-                                            sc, len(self.w.scalars), ctypes.byref(sd), h),
+        backend._check(L.acs_launch_sharded(self.k.handle, backend.VARIANTS[self.variant], self._sched(), descs,
+                                            len(arrays), sc, len(scalars or self.w.scalars), ctypes.byref(sd), h),
                        f"acs_launch_sharded({self.k.kernel_id})")
-        if self.lo_flag or self.hi_flag:
-            backend._check(L.acs_signal(self.lo_flag, self.hi_flag, s + 1, h), "acs_signal")
+
+    def _enqueue_peer(self, s: int, h, timeout_ms: int, before_launch=None) -> None:
+        L = _fns()
+        neighbours = bool(self.lo_ptr or self.hi_ptr)
+        if neighbours:
+            backend._check(L.acs_wait_ctr(self.flags.data_ptr() if self.lo_ptr else None,
+                                          self.flags.data_ptr() + 8 if self.hi_ptr else None,
+                                          self.ctr.data_ptr(), timeout_ms, h), "acs_wait_ctr")
+        if before_launch is not None:
+            before_launch(s, h)
+        self._launch(s, h)
+        if neighbours:
+            backend._check(L.acs_signal_ctr(self.lo_flag, self.hi_flag, self.ctr.data_ptr(), h), "acs_signal_ctr")
+
+    def _step_p2p(self, s: int, stream, before_launch=None) -> None:
+        """Boundary planes, then their exchange on the comm stream overlapped
+        with the interior planes."""
+        torch = self.torch
+        stream = stream or torch.cuda.current_stream()
+        h = backend._stream_handle(stream)
+        beg, end = self.w.spec.range_params
+        lo, hi = self.plan.local_range(self.rank)
+        halo = self.plan.halo
+        stream.wait_event(self.comm_done)               # halos of the previous step are in place
+        if before_launch is not None:
+            before_launch(s, h)
+        has_lo, has_hi = self.rank > 0, self.rank < self.nranks - 1
+        blo = lo + halo if has_lo else lo               # interior [blo, bhi)
+        bhi = hi - halo if has_hi else hi
+        sc = dict(self.w.scalars)
+        for a, b in ((lo, blo), (bhi, hi)):
+            if b > a:
+                sc[beg], sc[end] = a, b
+                self._launch(s, h, sc, write_through=False)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        out = role_buffers(self.nest, self.names, s)[self.w.write_arrays[0]]
+        with torch.cuda.stream(self.comm_stream):
+            self.comm_stream.wait_event(ev)
+            halo_exchange(self.dist, self.rank, self.nranks, self.buf[out], lo, hi, halo, self.group)
+            self.comm_done.record(self.comm_stream)
+        if bhi > blo:
+            sc[beg], sc[end] = blo, bhi
+            self._launch(s, h, sc, write_through=False)
+
+    def step(self, stream=None, timeout_ms: int = 20000, before_launch=None) -> None:
+        """One step: wait for the neighbours' previous step, compute the owned
+        planes with the exchange, signal the neighbours.  `before_launch(s,
+        stream_handle)` (eager steps only) enqueues work that must follow the
+        wait and precede the launch, e.g. host uploads into this rank's
+        buffers."""
+        s = self.step_no
+        if self.mode == "p2p":
+            self._step_p2p(s, stream, before_launch)
+        elif self.graphs is not None and before_launch is None:
+            with self.torch.cuda.stream(stream or self.torch.cuda.current_stream()):
+                self.graphs[s % self.period].replay()
+        else:
+            self._enqueue_peer(s, backend._stream_handle(stream), timeout_ms, before_launch)
         self.step_no = s + 1
+
+    def capture(self, stream=None, timeout_ms: int = 20000) -> None:
+        """Captures one CUDA graph per rotation phase of the peer-memory step
+        (wait_ctr, launch with write-through, signal_ctr); ``step`` then
+        replays them.  The device counter carries the step number."""
+        if self.mode == "p2p":
+            raise RuntimeError("capture: the message-passing step is not captured (NCCL P2P owns its streams)")
+        torch = self.torch
+        stream = stream or torch.cuda.current_stream()
+        cs = torch.cuda.Stream()
+        graphs = []
+        torch.cuda.synchronize()
+        for phase in range(self.period):
+            g = torch.cuda.CUDAGraph()
+            cs.wait_stream(stream)
+            with torch.cuda.graph(g, stream=cs):
+                self._enqueue_peer(phase, backend._stream_handle(cs), timeout_ms)
+            graphs.append(g)
+        stream.wait_stream(cs)
+        torch.cuda.synchronize()
+        self.graphs = graphs
 
     def current(self, name: str):
         """Physical buffer holding parameter `name` after the steps so far."""
-        return self.buf[role_buffers(self.nest, [a.name for a in self.w.spec.arrays], self.step_no)[name]]
+        return self.buf[role_buffers(self.nest, self.names, self.step_no)[name]]
 
     def owned_slice(self, name: str):
         """This rank's owned planes of parameter `name` (device tensor view)."""

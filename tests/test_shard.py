@@ -2,10 +2,12 @@
 
 * SlabPlan partitions the outermost loop exactly and sizes local buffers;
 * buffer rotation matches the nests' ping-pong / 3-level schemes;
-* an emulation of owner-computes + halo write-through with world_size 2 over
-  the gloo backend, each rank running the CPU oracle on its slab, reproduces
-  the single-domain result bit for bit (the device path does the same
-  forwarding from inside the kernel; tests/test_gpu_shard.py checks that)."""
+* world_size 2 and 3 over the gloo backend: each rank runs the CPU oracle on
+  its slab and exchanges the produced boundary planes with
+  ``shard.halo_exchange`` — the code the device path runs over NCCL when peer
+  memory is unavailable — and the gathered result equals the single-domain
+  run bit for bit (the peer-memory write-through path is checked on the
+  device by tests/test_gpu_shard.py)."""
 import os
 import socket
 
@@ -55,6 +57,9 @@ def _free_port():
 
 
 def _worker(rank, nranks, port, kid, size, steps, q):
+    """One rank: the CPU oracle on its slab (local loop bounds), then the
+    produced array's boundary planes exchanged through shard.halo_exchange —
+    the same function the device path runs over NCCL (connect_p2p)."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=nranks)
     w = nests.workload(kid, size)
@@ -65,33 +70,14 @@ def _worker(rank, nranks, port, kid, size, steps, q):
     n = plan.local_planes(rank)
     loc = {k: np.ascontiguousarray(v[o:o + n]).copy() for k, v in g.items()}
     lo, hi = plan.owned(rank)
+    llo, lhi = plan.local_range(rank)
     names = [a.name for a in w.spec.arrays]
     for s in range(steps):
         roles = shard.role_buffers(w.spec.nest, names, s)
         arrs = {p: loc[b] for p, b in roles.items()}
         oracle_cpu.run(w.spec, arrs, lw.scalars, "accsat", fma=True)
-        # write-through of the produced array's boundary planes (whole planes:
-        # the owner rewrites every element of its owned planes each step)
         out = roles[w.write_arrays[0]]
-        h = plan.halo
-        reqs = []
-        if rank > 0:
-            reqs.append(dist.isend(torch.from_numpy(loc[out][lo - o:lo - o + h].copy()), rank - 1))
-        if rank < nranks - 1:
-            reqs.append(dist.isend(torch.from_numpy(loc[out][hi - o - h:hi - o].copy()), rank + 1))
-        if rank > 0:
-            buf = torch.from_numpy(np.empty_like(loc[out][:h]))
-            dist.recv(buf, rank - 1)
-            lo_o = plan.origin(rank - 1)
-            lo_hi = plan.owned(rank - 1)[1]
-            loc[out][lo_hi - h - o:lo_hi - o] = buf.numpy()
-        if rank < nranks - 1:
-            buf = torch.from_numpy(np.empty_like(loc[out][:h]))
-            dist.recv(buf, rank + 1)
-            up_lo = plan.owned(rank + 1)[0]
-            loc[out][up_lo - o:up_lo + h - o] = buf.numpy()
-        for r in reqs:
-            r.wait()
+        shard.halo_exchange(dist, rank, nranks, torch.from_numpy(loc[out]), llo, lhi, plan.halo)
     latest = {"jacobi7": "A0", "wave4": "u", "d3q19": "src"}[w.spec.nest]   # holds the newest field
     final = shard.role_buffers(w.spec.nest, names, steps)[latest]
     part = loc[final][lo - o:hi - o]
@@ -102,9 +88,31 @@ def _worker(rank, nranks, port, kid, size, steps, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kid,size,steps", [("jacobi7.c:jacobi7:0", (9, 6, 7), 3), ("wave4.c:wave4:0", (11, 5, 6), 4)])
-def test_gloo_two_ranks_equal_single_domain(kid, size, steps):
-    nranks = 2
+def test_exchange_ops():
+    assert shard.exchange_ops(0, 1, 2, 10, 2) == []
+    assert shard.exchange_ops(0, 3, 2, 10, 2) == [(1, (8, 10), (10, 12))]
+    assert shard.exchange_ops(1, 3, 2, 10, 2) == [(0, (2, 4), (0, 2)), (2, (8, 10), (10, 12))]
+    assert shard.exchange_ops(2, 3, 1, 5, 0) == []
+
+
+def test_plane_view_covers_padded_planes():
+    t = torch.arange(5 * 3 * 8, dtype=torch.float64).reshape(5, 3, 8)[:, :, :6]   # padded pitch
+    v = shard.plane_view(t, 1, 3)
+    assert v.is_contiguous() and v.numel() == 8 * 3 + 2 * 8 + 6
+    assert v[0].item() == t[1, 0, 0].item() and v[-1].item() == t[2, 2, 5].item()
+
+
+def test_plan_rejects_thin_slabs():
+    w = nests.workload("wave4.c:wave4:0", (5, 4, 4))
+    with pytest.raises(ValueError):
+        shard.plan_for(w, 3)      # 1-plane slabs, halo 2
+    shard.plan_for(w, 2)
+
+
+@pytest.mark.parametrize("kid,size,steps,nranks", [("jacobi7.c:jacobi7:0", (9, 6, 7), 3, 2),
+                                                 ("wave4.c:wave4:0", (11, 5, 6), 4, 2),
+                                                 ("wave4.c:wave4:0", (13, 5, 6), 5, 3)])
+def test_gloo_ranks_equal_single_domain(kid, size, steps, nranks):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
