@@ -471,46 +471,21 @@ def bench_kernel(kid, size, dtype, sweeps, variant, schedule, reps, warmup=3):
     """Device-resident GB/s of one nest at its BASELINE size (ping-pong / 3-level
     rotation where the nest has one); median and IQR over `reps` steps."""
     import torch
-    from paper_2306_13002_b200 import backend, nests
+    from paper_2306_13002_b200 import backend, nests, stepper
     w = nests.workload(kid, size, dtype=dtype)
     k = backend.Kernel.lookup(kid)
     arrs = nests.device_inputs(w, native=True, kernel=k)
-    sc = dict(w.scalars)
-    names = list(arrs)
     stream = torch.cuda.current_stream()
-    state = {"t": 0}
-    period = nests.rotation_period(w.spec.nest)
-
-    def launch(t, st):
-        roles = nests.role_buffers(w.spec.nest, names, t)
-        k.launch({p: arrs[b] for p, b in roles.items()}, sc, variant, schedule, st)
-
-    def step():
-        for _ in range(sweeps):
-            launch(state["t"], stream)
-            state["t"] += 1
-
-    run = step
-    if sweeps > 1 and sweeps % period == 0:
+    st = stepper.Stepper(k, arrs, w.scalars, variant, schedule, sweeps)
+    if sweeps > 1:
         # a multi-sweep step (Jacobi: 100 ping-pong sweeps) is one CUDA graph
         # of `sweeps` kernel launches, captured once and replayed: the
         # per-launch host cost leaves the timed region, as in a real time loop
-        for _ in range(warmup):
-            step()
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        cs = torch.cuda.Stream()
-        cs.wait_stream(stream)
-        with torch.cuda.graph(g, stream=cs):
-            for t in range(sweeps):
-                launch(t, cs)
-        stream.wait_stream(cs)
-        torch.cuda.synchronize()
-        run = g.replay
-    ms = time_reps(run, reps, warmup, stream)
+        st.capture(stream)
+    ms = time_reps(lambda: st.step(stream), reps, warmup, stream)
     med, iqr = stats(ms)
     gbs = w.algorithmic_bytes * sweeps / (med * 1e-3) / 1e9
-    del arrs
+    del arrs, st
     torch.cuda.empty_cache()
     return {"ms": round(med, 4), "iqr_ms": round(iqr, 4), "gbs": round(gbs, 1)}, w
 

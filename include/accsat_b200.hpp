@@ -172,9 +172,14 @@ struct DiffReport {
     bool ok() const { return failures == 0; }
 };
 
-inline DiffReport diff_envs(const Environment& want, const Environment& got, double tol_rel, double abs_floor = 1e-12) {
+// nan_equal: NaN matches NaN (any payload) and an infinity matches the same
+// infinity — for edge-value inputs, where the reference rule (NaN always
+// fails) cannot tell a faithful executor from a broken one.
+inline DiffReport diff_envs(const Environment& want, const Environment& got, double tol_rel, double abs_floor = 1e-12,
+                            bool nan_equal = false) {
     DiffReport rep;
     auto value = [&](double w, double g) {
+        if (nan_equal && ((std::isnan(w) && std::isnan(g)) || (std::isinf(w) && w == g))) return;
         const double ae = std::fabs(g - w), mag = std::max(std::fabs(g), std::fabs(w));
         const double re = mag > 0.0 ? ae / mag : 0.0;
         rep.max_abs_err = std::max(rep.max_abs_err, ae);

@@ -70,6 +70,20 @@ int main() {
             ++fails;
         }
     }
+    // comparator modes: NaN always fails the reference rule; nan_equal accepts
+    // NaN vs NaN and equal infinities, and still rejects NaN vs a number
+    {
+        acs::Environment a, b, c;
+        a.scalars["x"] = acs::Scalar::of_double(std::nan(""));
+        b.scalars["x"] = acs::Scalar::of_double(-std::nan(""));
+        c.scalars["x"] = acs::Scalar::of_double(1.0);
+        a.scalars["y"] = b.scalars["y"] = c.scalars["y"] = acs::Scalar::of_double(HUGE_VAL);
+        if (acs::diff_envs(a, b, 1e-12).ok() || !acs::diff_envs(a, b, 1e-12, 1e-12, true).ok() ||
+            acs::diff_envs(a, c, 1e-12, 1e-12, true).ok()) {
+            std::printf("diff_envs nan_equal mode wrong\n");
+            ++fails;
+        }
+    }
     // EvalError contract: a missing array is an error, never a silent result
     acs::Environment bad = env;
     bad.arrays.erase("Anext");

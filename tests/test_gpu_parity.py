@@ -343,40 +343,5 @@ def test_empty_iteration_space_is_a_noop(kid, which):
             for n in ins:
                 assert bitwise_equal(got[n], ins[n]), f"{kid} {variant}/{sched} empty {which}: '{n}' changed"
 
-
-# ---- full BASELINE sizes: the GPU against the compiled reference text --------
-
-FULL = [("jacobi7.c:jacobi7:0", 256, "f64"), ("d3q19.c:stream_collide:0", 256, "f64"),
-        ("swim.c:calc1:0", 8192, "f64"), ("swim.c:calc2:1", 8192, "f64"), ("swim.c:calc3:2", 8192, "f64"),
-        ("clover.c:ideal_gas:0", 7680, "f64"), ("clover.c:pdv_predict:1", 7680, "f64"),
-        ("clover.c:advec_cell_x:2", 7680, "f64"), ("wave4.c:wave4:0", 512, "f32"),
-        ("zsolve.c:z_solve_lhs:0", 128, "f64")]
-
-
-@pytest.mark.parametrize("kid,size,dtype", FULL, ids=[f[0].split(":")[1] for f in FULL])
-def test_full_size_accsat_bitexact_vs_compiled_reference(kid, size, dtype):
-    """At the BASELINE grid (wave4 at 512^3 and zsolve at 128^3 to bound host
-    memory), one launch of the tuned accsat kernel equals the reference-emitted
-    accsat text compiled by gcc (FMA-rewritten, OpenMP) bit for bit."""
-    torch = _torch()
-    spec = nests.kernel(kid)
-    w = nests.workload(kid, size, dtype=dtype)
-    k = backend.Kernel.lookup(kid)
-    dev = nests.device_inputs(w, native=True, kernel=k)
-    host = {}
-    for n, t in dev.items():
-        host[n] = to_host(t)
-    k.tune(dev, dict(w.scalars), "accsat", reps=1)
-    dev = nests.device_inputs(w, native=True, kernel=k)       # fresh inputs after tuning
-    k.launch(dev, dict(w.scalars), "accsat", "default")
-    got = {n: to_host(t) for n, t in dev.items()}
-    del dev
-    torch.cuda.empty_cache()
-    want = {n: np.ascontiguousarray(a) for n, a in host.items()}
-    oracle_cpu.run(spec, want, w.scalars, "accsat", fma=True, f32=dtype == "f32", threads=os.cpu_count() or 1)
-    for n in w.write_arrays:
-        if not bitwise_equal(got[n], want[n]):
-            diff = np.flatnonzero(got[n].view(np.uint8).reshape(got[n].size, -1).any(axis=1)
-                                  != want[n].view(np.uint8).reshape(want[n].size, -1).any(axis=1))
-            raise AssertionError(f"{kid} full size: '{n}' differs from the compiled reference "
-                                 f"({diff.size} elements differ by zero-ness)")
+# Full BASELINE sizes (every form, naive + tuned slots, wave4 1024^3, zsolve 256^3,
+# the Jacobi graph step, the slab path, the e2e path) and edge values: tests/test_gpu_fullsize.py
