@@ -467,27 +467,45 @@ def tune_kernel(kid, size, dtype, variant):
     return best, name, ms
 
 
-def bench_kernel(kid, size, dtype, sweeps, variant, schedule, reps, warmup=3):
-    """Device-resident GB/s of one nest at its BASELINE size (ping-pong / 3-level
-    rotation where the nest has one); median and IQR over `reps` steps."""
+def bench_configs(kid, size, dtype, sweeps, configs, reps, warmup=3):
+    """Device-resident GB/s of one nest at its BASELINE size for several
+    (form, schedule) configurations, each on its own resident arrays, with the
+    repetitions INTERLEAVED (A B C A B C ...) so clock / power-cap drift hits
+    every configuration alike; median and IQR of `reps` CUDA-event-timed steps
+    each.  Buffers rotate like the nest's time loop (ping-pong / 3-level);
+    a multi-sweep step (Jacobi: 100 sweeps) is one CUDA graph, replayed."""
     import torch
     from paper_2306_13002_b200 import backend, nests, stepper
     w = nests.workload(kid, size, dtype=dtype)
     k = backend.Kernel.lookup(kid)
-    arrs = nests.device_inputs(w, native=True, kernel=k)
     stream = torch.cuda.current_stream()
-    st = stepper.Stepper(k, arrs, w.scalars, variant, schedule, sweeps)
-    if sweeps > 1:
-        # a multi-sweep step (Jacobi: 100 ping-pong sweeps) is one CUDA graph
-        # of `sweeps` kernel launches, captured once and replayed: the
-        # per-launch host cost leaves the timed region, as in a real time loop
-        st.capture(stream)
-    ms = time_reps(lambda: st.step(stream), reps, warmup, stream)
-    med, iqr = stats(ms)
-    gbs = w.algorithmic_bytes * sweeps / (med * 1e-3) / 1e9
-    del arrs, st
+    steppers = []
+    for variant, sched in configs:
+        arrs = nests.device_inputs(w, native=True, kernel=k)
+        st = stepper.Stepper(k, arrs, w.scalars, variant, sched, sweeps)
+        if sweeps > 1:
+            st.capture(stream)
+        steppers.append(st)
+    for _ in range(warmup):
+        for st in steppers:
+            st.step(stream)
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)] for _ in steppers]
+    for r in range(reps):
+        for i, st in enumerate(steppers):
+            ev[i][2 * r].record(stream)
+            st.step(stream)
+            ev[i][2 * r + 1].record(stream)
+    torch.cuda.synchronize()
+    out = []
+    for i in range(len(steppers)):
+        ms = [ev[i][2 * r].elapsed_time(ev[i][2 * r + 1]) for r in range(reps)]
+        med, iqr = stats(ms)
+        gbs = w.algorithmic_bytes * sweeps / (med * 1e-3) / 1e9
+        out.append({"ms": round(med, 4), "iqr_ms": round(iqr, 4), "gbs": round(gbs, 1)})
+    del steppers
     torch.cuda.empty_cache()
-    return {"ms": round(med, 4), "iqr_ms": round(iqr, 4), "gbs": round(gbs, 1)}, w
+    return out, w
 
 
 def per_kernel_table(peak, reps):
@@ -495,7 +513,8 @@ def per_kernel_table(peak, reps):
     for kid, size, dtype, sweeps in TABLE:
         fn = kid.split(":")[1]
         row = {"size": size, "dtype": dtype, "sweeps_per_step": sweeps, "reps": reps,
-               "timing": f"median and IQR of {reps} CUDA-event-timed steps"}
+               "timing": f"median and IQR of {reps} CUDA-event-timed steps per configuration, "
+                         "configurations interleaved rep by rep"}
         if sweeps > 1:
             row["launch"] = f"CUDA graph of {sweeps} kernel launches per step (every form alike)"
         slots = {}
@@ -507,20 +526,19 @@ def per_kernel_table(peak, reps):
                                            "ms_per_slot": {str(s): round(v, 4) for s, v in tms.items()}}
             except Exception as e:
                 row[f"tuned_{variant}"] = {"error": str(e)[:200]}
-        w = None
-        for variant, sched, key in (("original", "naive", "original/naive"),
-                                    ("original", slots.get("original"), "original/tuned"),
-                                    ("original-nvcc", "naive", "original-nvcc/naive"),
-                                    ("accsat", "naive", "accsat/naive"),
-                                    ("accsat", slots.get("accsat"), "accsat/tuned")):
-            if sched is None:
-                continue
-            try:
-                r, w = bench_kernel(kid, size, dtype, sweeps, variant, sched, reps)
+        keys = [("original", "naive", "original/naive"), ("original", slots.get("original"), "original/tuned"),
+                ("original-nvcc", "naive", "original-nvcc/naive"), ("accsat", "naive", "accsat/naive"),
+                ("accsat", slots.get("accsat"), "accsat/tuned")]
+        keys = [kk for kk in keys if kk[1] is not None]
+        try:
+            res, w = bench_configs(kid, size, dtype, sweeps, [(v, s) for v, s, _ in keys], reps)
+            for (_, _, key), r in zip(keys, res):
                 r["frac"] = round(r["gbs"] / peak, 4)
                 row[key] = r
-            except Exception as e:  # report, never hide
-                row[key] = {"error": str(e)[:200]}
+        except Exception as e:  # report, never hide
+            row["error"] = str(e)[:300]
+            rows[fn] = row
+            continue
         try:
             def ratio(a, b):
                 A, B = row[a], row[b]

@@ -6,9 +6,12 @@ bench.py's cpu_baseline / --impl reference legs, never by the product path.
 The library holds, for every nest function F and form:
   F__original        the nest text (nests/<nest>.c)            gcc -O3 -ffp-contract=off
   F__cse|cse_bulk|cse_sat|accsat
-                     the reference-emitted text for that VariantConfig
-                     (tests/golden/emitted/), two-rounding FMA as the
+                     host stage (a)'s emitted text for that VariantConfig
+                     (paper_2306_13002_b200/emitted/ — the program the GPU
+                     kernels are lowered from), two-rounding FMA as the
                      reference interpreter evaluates it (proj/src/interp.cpp:68-70)
+  F__ref_<form>      the same for the REFERENCE optimizer's emitted text
+                     (tests/golden/emitted/), the cross-check
   F__cse_sat_fma|accsat_fma
                      the same text with each extracted FMA as one fma() —
                      the arithmetic the sm_100a saturated kernels perform
@@ -34,6 +37,8 @@ _lib = None
 
 
 def build() -> str:
+    import sys
+    subprocess.run([sys.executable, os.path.join(HERE, "gen_oracle_c.py")], check=True, stdout=subprocess.DEVNULL)
     subprocess.run(["make", "-s", "-C", HERE, "cpu"], check=True)
     return LIB_PATH
 
@@ -47,8 +52,10 @@ def lib():
     return _lib
 
 
-def form_name(variant: str, fma: bool = False, f32: bool = False) -> str:
+def form_name(variant: str, fma: bool = False, f32: bool = False, ref: bool = False) -> str:
     f = FORM_OF_VARIANT[variant]
+    if ref and variant != "original":
+        f = "ref_" + f
     if fma and variant in ("cse+sat", "accsat"):
         f += "_fma"
     if f32:
@@ -57,10 +64,12 @@ def form_name(variant: str, fma: bool = False, f32: bool = False) -> str:
 
 
 def run(spec, arrays: Dict[str, np.ndarray], scalars: Dict[str, float], variant: str = "original",
-        fma: bool = False, f32: bool = False, threads: int = 0) -> None:
+        fma: bool = False, f32: bool = False, threads: int = 0, ref: bool = False) -> None:
     """Runs one nest function IN PLACE on host arrays (reference layout).
 
-    `spec` is a nests.KernelSpec; `threads` > 0 uses the OpenMP driver."""
+    `spec` is a nests.KernelSpec; `threads` > 0 uses the OpenMP driver;
+    `ref` runs the reference optimizer's emitted text for `variant` instead of
+    host stage (a)'s."""
     n = len(spec.params)
     a = (ctypes.c_void_p * n)()
     d = (ctypes.c_long * (8 * n))()
@@ -77,7 +86,7 @@ def run(spec, arrays: Dict[str, np.ndarray], scalars: Dict[str, float], variant:
             iv[p.position] = int(scalars[p.name])
         else:
             dv[p.position] = float(scalars[p.name])
-    sym = f"{spec.function}__{form_name(variant, fma, f32)}"
+    sym = f"{spec.function}__{form_name(variant, fma, f32, ref)}"
     if threads > 0:
         fn = getattr(lib(), sym + "_omp")
         fn.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int]

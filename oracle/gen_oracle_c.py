@@ -3,9 +3,19 @@
 
 What the oracle is: the reference's own way of running a nest at scale, i.e.
 wrapper mode ``satcc -- cc -O3 kernel.c`` (proj/tools/satcc_main.cpp:285-360):
-the nest text (original form) or the text the reference optimizer emitted
-(tests/golden/emitted/<nest>.<variant>.c, frozen by tools/gen_goldens.py) is
-handed to a C compiler.  This script makes only MECHANICAL edits to that text:
+the nest text (original form) or an optimizer's emitted text is handed to a C
+compiler.  Two emitted sets are compiled:
+
+  * ``<form>``      the text host stage (a) emitted — this repo's optimizer
+                    (paper_2306_13002_b200/emitted/, stage_a.py): the SAME
+                    program the sm_100a kernels are lowered from, so GPU and
+                    checker run one text;
+  * ``ref_<form>``  the text the UNMODIFIED reference optimizer emitted
+                    (tests/golden/emitted/<nest>.<variant>.c, frozen by
+                    tools/gen_goldens.py): the cross-check that our forms
+                    compute what the reference's forms compute.
+
+This script makes only MECHANICAL edits to those texts:
 
   1. each function is renamed ``<fn>__<form>`` and its fixed-dim array
      parameters become C99 VLA parameters ``double A[][d1][d2]`` so a single
@@ -33,6 +43,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 sys.path.insert(0, ROOT)
 from paper_2306_13002_b200 import kernel_subset as ks  # noqa: E402
+from paper_2306_13002_b200 import stage_a  # noqa: E402
 
 NESTS = ["jacobi7", "swim", "clover", "wave4", "d3q19", "zsolve"]
 F32_NESTS = {"wave4"}
@@ -40,6 +51,7 @@ F32_NESTS = {"wave4"}
 FORMS = [("original", None, False), ("cse", "cse", False), ("cse_bulk", "cse+bulk", False),
          ("cse_sat", "cse+sat", False), ("cse_sat_fma", "cse+sat", True),
          ("accsat", "accsat", False), ("accsat_fma", "accsat", True)]
+FORMS = FORMS + [("ref_" + f, v, fma) for f, v, fma in FORMS if v is not None]
 
 FMA_RE = re.compile(r"^(\s*)(_v\d+) = ([A-Za-z_]\w*|-?[0-9.][0-9.eE+-]*) \+ "
                     r"([A-Za-z_]\w*|-?[0-9.][0-9.eE+-]*) \* ([A-Za-z_]\w*|-?[0-9.][0-9.eE+-]*);$")
@@ -163,15 +175,20 @@ def to_f32(text):
 
 def generate(nest):
     files = {}
-    parts = [f"/* GENERATED by oracle/gen_oracle_c.py from nests/{nest}.c and the reference-emitted\n"
-             f" * tests/golden/emitted/{nest}.<variant>.c — TEST INFRASTRUCTURE ONLY (CPU oracle).\n"
+    parts = [f"/* GENERATED by oracle/gen_oracle_c.py from nests/{nest}.c, the stage (a) texts\n"
+             f" * paper_2306_13002_b200/emitted/{nest}.<variant>.c and the reference-emitted\n"
+             f" * tests/golden/emitted/{nest}.<variant>.c (ref_ forms) — TEST INFRASTRUCTURE ONLY.\n"
              " * Bodies are the reference text verbatim; see the generator for the only edits. */\n",
              '#include "acs_cpu.h"\n']
     f32 = [p for p in parts]
     fma_counts = {}
     for form, variant, fma in FORMS:
-        path = (os.path.join(ROOT, "nests", f"{nest}.c") if variant is None else
-                os.path.join(ROOT, "tests", "golden", "emitted", f"{nest}.{variant}.c"))
+        if variant is None:
+            path = os.path.join(ROOT, "nests", f"{nest}.c")
+        elif form.startswith("ref_"):
+            path = os.path.join(ROOT, "tests", "golden", "emitted", f"{nest}.{variant}.c")
+        else:
+            path = stage_a.ensure(nest, variant)
         text = open(path).read()
         text = re.sub(r"/\*.*?\*/\n?", "", text, flags=re.S)
         for fname, params, body in split_functions(text):

@@ -1,9 +1,10 @@
 """Lowers a nest function (kernel-subset C) to sm_100a device code.
 
 This is the backend's compile stage for the execution path: it takes a nest
-text — the ORIGINAL source (nests/<nest>.c) or a form EMITTED by the
-reference optimizer (tests/golden/emitted/<nest>.<variant>.c, the
-``optimize_source`` output of proj/src/pipeline.cpp:140-194) — and produces,
+text — the ORIGINAL source (nests/<nest>.c) or a form EMITTED by host stage
+(a), this repo's re-implementation of the reference optimizer
+(paper_2306_13002_b200/emitted/<nest>.<variant>.c, written by stage_a.py; the
+``optimize_source`` contract of proj/src/pipeline.cpp:140-194) — and produces,
 per registered region, a ``__device__`` per-point body.  The hand-written
 kernel skeletons (csrc/kernels/*.cuh) decide the thread mapping and where each
 array element comes from (global memory, a shared-memory tile, a register
@@ -39,6 +40,7 @@ from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Tuple
 
 from . import kernel_subset as ks
+from . import stage_a
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -941,8 +943,7 @@ def gen_function(nest: str, function: str, f32: bool = False) -> Tuple[str, dict
     ns = function + ("_f32" if f32 else "")
     texts = {}
     for form, variant, fma in FORMS:
-        path = (os.path.join(ROOT, "nests", f"{nest}.c") if variant is None
-                else os.path.join(ROOT, "tests", "golden", "emitted", f"{nest}.{variant}.c"))
+        path = os.path.join(ROOT, "nests", f"{nest}.c") if variant is None else stage_a.ensure(nest, variant)
         texts[form] = (open(path).read(), fma)
     lows = {form: lower_text(t, function, fma, f32) for form, (t, fma) in texts.items()}
     base = lows["original"]
@@ -1220,8 +1221,8 @@ def generate_all(out_dir: str) -> dict:
     allmeta = {}
     for nest, fns in NEST_FUNCS.items():
         parts = ["// GENERATED by paper_2306_13002_b200/lowering.py from nests/" + nest +
-                 ".c (original form) and tests/golden/emitted/" + nest + ".<variant>.c",
-                 "// (reference-emitted forms).  Do not edit: re-run `python -m "
+                 ".c (original form) and paper_2306_13002_b200/emitted/" + nest + ".<variant>.c",
+                 "// (host stage (a): this repo's optimizer, stage_a.py).  Do not edit: re-run `python -m "
                  "paper_2306_13002_b200.lowering`.",
                  "#pragma once", "namespace acs { namespace gen {"]
         for fn in fns:

@@ -1,0 +1,75 @@
+"""Host stage (a) at build time: the forms the sm_100a kernels execute.
+
+For every benchmark nest (``nests/<nest>.c``, the ORIGINAL form) and every
+``VariantConfig`` (cse, cse+sat, cse+bulk, accsat), this repo's own C++
+optimizer (``host/acs_opt.cpp`` through ``satopt.optimize_source`` — the
+re-implementation of the reference's ``optimize_source``,
+proj/src/pipeline.cpp:140-194) emits the saturated module text and its
+satcc-metrics-v1 metrics into ``paper_2306_13002_b200/emitted/``.  The
+lowering (``lowering.py``) turns those texts into the device bodies, and the
+CPU checker (``oracle/gen_oracle_c.py``) compiles the same texts, so the GPU
+and its oracle always run the same program.
+
+The reference optimizer's own output for the same inputs stays frozen under
+``tests/golden/emitted/`` as a cross-check only (tests/test_opt.py: our
+objective is never worse; tests/test_gpu_stage_a.py: the GPU running our
+forms agrees with the reference-emitted forms compiled by gcc).
+
+    python -m paper_2306_13002_b200.stage_a      # (re)writes emitted/
+"""
+from __future__ import annotations
+
+import json
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+OUT_DIR = os.path.join(HERE, "emitted")
+NESTS = ["jacobi7", "swim", "clover", "wave4", "d3q19", "zsolve"]
+VARIANTS = ["cse", "cse+sat", "cse+bulk", "accsat"]
+
+
+def emitted_path(nest: str, variant: str, kind: str = "c") -> str:
+    return os.path.join(OUT_DIR, f"{nest}.{variant}.{kind}")
+
+
+def emit(nest: str, variant: str) -> dict:
+    from . import satopt
+    src = open(os.path.join(ROOT, "nests", f"{nest}.c")).read()
+    text, meta = satopt.optimize_source(src, f"{nest}.c", variant)
+    bad = [r for r in meta["regions"] if r.get("error")]
+    if bad:
+        raise RuntimeError(f"stage (a) failed on {nest}.c ({variant}): {bad[0]['error']}")
+    os.makedirs(OUT_DIR, exist_ok=True)
+    with open(emitted_path(nest, variant), "w") as f:
+        f.write(text)
+    with open(emitted_path(nest, variant, "json"), "w") as f:
+        json.dump(meta, f, indent=1)
+    return meta
+
+
+def emit_all() -> dict:
+    return {(n, v): emit(n, v) for n in NESTS for v in VARIANTS}
+
+
+def ensure(nest: str, variant: str) -> str:
+    """Path of the emitted text, generating it when missing or older than the
+    nest text."""
+    p = emitted_path(nest, variant)
+    src = os.path.join(ROOT, "nests", f"{nest}.c")
+    if not os.path.exists(p) or os.path.getmtime(p) < os.path.getmtime(src):
+        emit(nest, variant)
+    return p
+
+
+def metrics(nest: str, variant: str) -> dict:
+    ensure(nest, variant)
+    with open(emitted_path(nest, variant, "json")) as f:
+        return json.load(f)
+
+
+if __name__ == "__main__":
+    for (n, v), m in emit_all().items():
+        for r in m["regions"]:
+            print(f"{n:8s} {v:9s} {r['function']:15s} objective {r['objective_before']} -> {r['objective_after']}, "
+                  f"loads {r['static_loads_before']} -> {r['static_loads_after']}, fma {r['fma_count']}")

@@ -38,11 +38,15 @@ def test_vectors_present():
 
 @pytest.mark.parametrize("path", VECTORS, ids=[os.path.basename(p)[:-4] for p in VECTORS])
 @pytest.mark.parametrize("variant", VARIANTS)
-def test_oracle_matches_reference_interpreter(path, variant):
+@pytest.mark.parametrize("text", ["stage_a", "reference"])
+def test_oracle_matches_reference_interpreter(path, variant, text):
+    """Both emitted texts — host stage (a)'s (what the GPU runs) and the
+    reference optimizer's — compiled by gcc give the reference interpreter's
+    results bit for bit (two-rounding FMA, as the interpreter evaluates it)."""
     spec, scalars, ins, outs = load(path)
     arrays = {k: np.ascontiguousarray(v.astype(np.int32) if v.dtype.kind == "i" else v.copy())
               for k, v in ins.items()}
-    oracle_cpu.run(spec, arrays, scalars, variant)
+    oracle_cpu.run(spec, arrays, scalars, variant, ref=text == "reference")
     prefix = f"{variant}_"
     checked = 0
     for key, want in outs.items():
@@ -85,3 +89,37 @@ def test_host_fill_matches_make_inputs(kid, size, dtype):
         assert got[n].dtype == want[n].dtype and got[n].shape == want[n].shape, n
         u = {8: np.uint64, 4: np.uint32}[want[n].itemsize]
         assert np.array_equal(got[n].view(u), want[n].view(u)), n
+
+
+CROSS = [("jacobi7.c:jacobi7:0", (6, 7, 9)), ("d3q19.c:stream_collide:0", (4, 5, 7)), ("swim.c:calc1:0", (9, 11)),
+         ("swim.c:calc2:1", (9, 11)), ("swim.c:calc3:2", (9, 11)), ("clover.c:ideal_gas:0", (7, 9)),
+         ("clover.c:pdv_predict:1", (7, 9)), ("clover.c:advec_cell_x:2", (7, 9)), ("wave4.c:wave4:0", (6, 5, 9)),
+         ("zsolve.c:z_solve_lhs:0", (3, 4, 5))]
+
+
+@pytest.mark.parametrize("kid,size", CROSS, ids=[c[0].split(":")[1] for c in CROSS])
+@pytest.mark.parametrize("variant", ["cse", "cse+bulk", "cse+sat", "accsat"])
+@pytest.mark.parametrize("fma", [False, True])
+def test_stage_a_forms_compute_what_reference_forms_compute(kid, size, variant, fma):
+    """Host stage (a)'s emitted form vs the reference optimizer's emitted form
+    of the same VariantConfig, both compiled, on the BASELINE input
+    distributions: the CSE-only forms bit for bit (CSE never changes
+    arithmetic); the saturated forms within the reference comparator rule
+    (rel 1e-12 or abs 1e-12, proj/src/oracle.cpp:12,36) — with real
+    single-rounding FMAs (fma=True, what the GPU computes) too."""
+    if fma and variant not in ("cse+sat", "accsat"):
+        pytest.skip("no FMA in the CSE-only forms")
+    spec = nests.kernel(kid)
+    w = nests.workload(kid, size)
+    ins = nests.make_inputs(w)
+    ours = {n: a.copy() for n, a in ins.items()}
+    theirs = {n: a.copy() for n, a in ins.items()}
+    oracle_cpu.run(spec, ours, w.scalars, variant, fma=fma)
+    oracle_cpu.run(spec, theirs, w.scalars, variant, fma=fma, ref=True)
+    for n in w.write_arrays:
+        a, b = ours[n], theirs[n]
+        if variant in ("cse", "cse+bulk"):
+            assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), n
+        else:
+            d = np.abs(a - b)
+            assert np.all((d <= 1e-12 * np.maximum(np.abs(a), np.abs(b))) | (d <= 1e-12)), (n, float(d.max()))
