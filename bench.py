@@ -601,7 +601,7 @@ def run_cpu_steps(w, variant, steps, threads, arrays):
         roles = nests.role_buffers(w.spec.nest, names, s)
         a = {p: arrays[roles[p]] for p in names}
         t0 = time.perf_counter()
-        oracle_cpu.run(w.spec, a, w.scalars, variant, threads=threads, f32=w.dtype == "f32")
+        oracle_cpu.run(w.spec, a, w.scalars, variant, threads=threads, f32=w.dtype == "f32", ref=True)
         ts.append(time.perf_counter() - t0)
     return ts
 

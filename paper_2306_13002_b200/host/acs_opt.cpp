@@ -1656,12 +1656,15 @@ struct Emitter {
         std::vector<int> here;
         for (auto& [c, p] : place)
             if (p.block == blk && p.slot == slot) here.push_back(c);
-        // dependency order; loads first (sorted by base, subscript text), then by class id
+        // dependency order, the reference's bulk-block layout: integer
+        // (subscript) temps first, then loads sorted by (base, subscript
+        // text), then the arithmetic by class id — each step emits the
+        // lowest-keyed temp whose operands are ready
         std::set<int> done;
         auto key = [&](int c) {
             const Node& n = x.choice.at(c);
             bool ld = n.op == Op::Load;
-            return std::make_tuple(ld ? 0 : 1, ld ? rhs_text(c) : std::string(), c);
+            return std::make_tuple(ld ? 1 : (g.is_int(c) ? 0 : 2), ld ? rhs_text(c) : std::string(), c);
         };
         std::sort(here.begin(), here.end(), [&](int a, int b2) { return key(a) < key(b2); });
         std::set<int> hs(here.begin(), here.end());
