@@ -32,6 +32,7 @@
 //    orders loads sharing a slot by (base, subscript text).  FMA temps print
 //    as `a + b * c` (the reference convention, proj/src/printer.cpp:114-125).
 #include <algorithm>
+#include <cctype>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -1175,7 +1176,21 @@ struct Builder {
     std::vector<RootUse> roots;
     std::vector<PhiInfo> phis;
     std::map<const Stmt*, int> cond_cls;
-    int scope_ctr = 0, scope = 0;
+    int scope_ctr = 0, scope = 0, loop_ctr = 0;
+
+    // scalars a loop assigns (header and body) and array bases it stores to
+    void scan_loop(const Stmt& s, std::set<std::string>& vars, std::set<std::string>& bases) {
+        if (s.k == Stmt::Assign) {
+            if (s.lhs->k == Expr::Var) vars.insert(s.lhs->text);
+            else bases.insert(s.lhs->text);
+        }
+        if (s.k == Stmt::Decl)
+            for (auto& d : s.decls)
+                if (d.dims.empty()) vars.insert(d.name);
+        for (const Stmt* c : {s.then_s.get(), s.else_s.get(), s.init.get(), s.step.get(), s.body.get()})
+            if (c) scan_loop(*c, vars, bases);
+        for (auto& c : s.stmts) scan_loop(*c, vars, bases);
+    }
 
     explicit Builder(EGraph& gg) : g(gg) {}
 
@@ -1364,7 +1379,29 @@ struct Builder {
                 scope = saved;
                 break;
             }
-            case Stmt::For: throw Unsupported("inner loops inside a region (left untouched)");
+            case Stmt::For: {
+                // a sequential loop inside the region (gated SSA for-/exit-φ,
+                // proj/src/ssa.cpp:487-549): every scalar the loop assigns is
+                // an opaque for-φ inside the body and an exit-φ after it; a
+                // base the loop stores to starts a new load epoch on entry
+                // (later iterations see the stores) and on exit
+                std::set<std::string> vars, bases;
+                scan_loop(s, vars, bases);
+                for (auto& bname : bases) events[bname].push_back({-1, {}, -1});
+                const int id = ++loop_ctr;
+                int saved = scope;
+                scope = ++scope_ctr;
+                for (auto& v : vars) env[v] = leaf(Op::Phi, v, sym(v).is_int, 2 * id);
+                if (s.body) stmt(*s.body);
+                scope = saved;
+                for (auto& v : vars) {
+                    int p = leaf(Op::Phi, v, sym(v).is_int, 2 * id + 1);
+                    env[v] = p;
+                    phis.push_back({p, v, &s});
+                }
+                for (auto& bname : bases) events[bname].push_back({-1, {}, -1});
+                break;
+            }
             case Stmt::Call:
             case Stmt::Empty: break;
         }
@@ -1433,6 +1470,10 @@ struct Emitter {
         } else if (s.k == Stmt::Block) {
             // nested plain block: index its contents as a child block
             then_block[&s] = index_block(s, blk, slot);
+        } else if (s.k == Stmt::For && s.body) {
+            // sequential inner loop: its body is a child block (temps of
+            // for-φ values stay inside it)
+            then_block[&s] = index_block(*s.body, blk, slot);
         }
     }
     std::vector<int> chain(int blk) {   // block, parent, ..., root
@@ -1759,7 +1800,19 @@ struct Emitter {
                 break;
             case Stmt::Call: o << ind << verbatim(s.beg, s.end) << "\n"; break;
             case Stmt::Empty: o << ind << ";\n"; break;
-            case Stmt::For: throw Unsupported("inner loop");
+            case Stmt::For: {
+                // header verbatim (init; cond; step), body re-emitted
+                std::string head = verbatim(s.beg, s.body ? s.body->beg : s.end);
+                while (!head.empty() && std::isspace((unsigned char)head.back())) head.pop_back();
+                o << ind << head << " {\n";
+                if (s.body) emit_list(then_block[&s], depth + 1, o, false);
+                o << ind << "}\n";
+                for (auto& p : b.phis)
+                    if (p.after_if == &s && atom_name.count(g.find(p.cls)))
+                        o << ind << (g.is_int(p.cls) ? "int " : "double ") << atom_name[g.find(p.cls)] << " = "
+                          << p.var << ";\n";
+                break;
+            }
         }
     }
 };

@@ -69,20 +69,55 @@ def test_unparseable_source_raises():
         satopt.optimize_source("void f( {", "bad.c", "accsat")
 
 
-def test_inner_loop_region_left_untouched():
-    src = """double a[8];
+def test_inner_loop_region_optimized():
+    """A sequential loop inside a region (gated SSA for-/exit-φ): the
+    loop-carried accumulation becomes one FMA, as the reference does for its
+    corpus matmul / dotacc / seqscan; loop headers stay verbatim."""
+    src = """double a[8][4];
+double b[4];
+double out[8];
 void f(void) {
     int i, j;
+    double s;
     #pragma acc parallel loop gang
     for (i = 0; i < 8; i++) {
-        for (j = 0; j < 2; j++) {
-            a[i] = a[i] + 1.0;
+        s = 0.0;
+        for (j = 0; j < 4; j++) {
+            s = s + a[i][j] * b[j];
         }
+        out[i] = s;
     }
 }
 """
     text, meta = satopt.optimize_source(src, "inner.c", "accsat")
-    assert text == src and meta["regions"][0]["error"]
+    r = meta["regions"][0]
+    assert r["error"] == "" and r["fma_count"] == 1 and r["objective_after"] < r["objective_before"]
+    assert "for (j = 0; j < 4; j++) {" in text
+
+
+def test_inner_loop_store_starts_new_epoch():
+    """A load after a loop that stores to the same base is not CSE'd with the
+    one before it (the stores of any iteration may alias it)."""
+    src = """double a[9];
+double out[9];
+void f(void) {
+    int i, j;
+    double x;
+    #pragma acc parallel loop gang
+    for (i = 0; i < 8; i++) {
+        x = a[i];
+        for (j = 0; j < 3; j++) {
+            a[i] = a[i] + 1.0;
+        }
+        out[i] = a[i] + x;
+    }
+}
+"""
+    text, meta = satopt.optimize_source(src, "epoch.c", "accsat")
+    assert meta["regions"][0]["error"] == ""
+    assert meta["regions"][0]["static_loads_after"] == 3      # before, inside, after the loop
+    ok, rep = satopt.verify_source(src, "epoch.c", "accsat", trials=5)
+    assert ok, rep
 
 
 needs_ref = pytest.mark.skipif(not os.path.exists(REF_TOOL), reason="oracle/_ref/ref_tool not built (needs /root/reference)")
