@@ -1,0 +1,41 @@
+"""compute-sanitizer over every skeleton (race detection).
+
+tests/sanitize_workload.py launches every registered schedule slot of every
+nest on small ragged grids — the TMA march ring with its mbarriers, the
+register-window march, the cp.async stream ring, the sliced register queue,
+the naive skeleton — plus a 2-slab sharded time loop on one device (peer
+write-through stores ordered by device flags, graph-replayed) and the
+host-buffer pipeline, and checks each against the CPU oracle.  Here it runs
+under memcheck (out-of-bounds / misaligned global and shared accesses),
+racecheck (shared-memory hazards) and synccheck (barrier misuse); every tool
+must report zero errors.
+"""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer_clean(tool):
+    assert os.path.exists(SAN), "compute-sanitizer not found"
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "99", "--print-limit", "20"]
+    if tool == "memcheck":
+        cmd += ["--leak-check", "no"]
+    cmd += [sys.executable, os.path.join(ROOT, "tests", "sanitize_workload.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=3000, cwd=ROOT)
+    out = r.stdout + r.stderr
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"sanitizer_{tool}.log"), "w") as f:
+        f.write(out)
+    assert "sanitize workload ok" in out, out[-3000:]
+    clean = ("RACECHECK SUMMARY: 0 hazards displayed (0 errors, 0 warnings)" if tool == "racecheck"
+             else "ERROR SUMMARY: 0 errors")
+    assert r.returncode == 0 and clean in out, out[-3000:]
