@@ -565,6 +565,227 @@ __device__ __forceinline__ void march_issue(unsigned char* slot_base, const TmaM
     }
 }
 
+// ---- one point per thread column (RX == 1): hoisted addressing ---------------
+//
+// Everything about a thread's points that does not change along the march is
+// computed once per thread: its element offset inside every staged box and
+// its global address in every statically stored (or unstaged loaded) array.
+// Per march step only the shared-memory address of each ring plane the body
+// reads (one add per array and plane) and the global pointers (one add per
+// array) move; the body's static loads are then one LDS at a compile-time byte
+// offset and its stores one STG at a per-thread constant offset — instead of
+// re-deriving the ring slot, the box index and a 64-bit subscript product per
+// load and store of every point (jacobi7: 74 -> see profiles/r02_jacobi.md).
+template <class NS, class T, class P, int MS>
+struct FastState {
+    unsigned plane[NS::NARR][MS > 0 ? MS : 1];   // byte offset (from the ring) of the thread's first point, per plane
+    unsigned stat[NS::NARR];                     // same in the static (plane-less) boxes
+    char* gp[NS::NARR];                          // global address of the thread's first point at plane k
+    long long gstep[NS::NARR];                   // bytes per march step
+
+    // arrays the body stores with static subscripts in form FORM
+    static constexpr bool stored_static(int a, int form) {
+        for (int r = 0; r < NS::NSROW; ++r)
+            if (NS::srow_arr(r) == a && ((NS::srow_forms(r) >> form) & 1)) return true;
+        return false;
+    }
+    static constexpr bool needs_gp(int a, int form) {
+        return stored_static(a, form) || (!P::staged(a) && NS::is_loaded(a));
+    }
+    // the body of form `form` reads array a at the thread's own inner
+    // coordinates in march plane dz (a static-load row with every non-march
+    // offset 0 whose x range covers 0)
+    static constexpr bool column(int a, int dz, int form) {
+        const int mp = P::march_pos(a);
+        for (int r = 0; r < NS::NROW; ++r) {
+            if (NS::row_arr(r) != a || !((NS::row_forms(r) >> form) & 1)) continue;
+            if (NS::row_xlo(r) > 0 || NS::row_xhi(r) < 0) continue;
+            bool ok = NS::row_off(r, mp) == dz;
+            for (int p = 0; p < NS::ndim(a); ++p)
+                if (p != mp && NS::row_off(r, p) != 0) ok = false;
+            if (ok) return true;
+        }
+        return false;
+    }
+    // every load of the body comes from a staged box (no global, no dynamic
+    // index): a point outside the domain can run the body on in-box values
+    // and just skip its stores — no branch per point
+    static constexpr bool all_staged() {
+        if (NS::has_dynamic_index) return false;
+        for (int a = 0; a < NS::NARR; ++a)
+            if (NS::is_loaded(a) && !P::staged(a)) return false;
+        return true;
+    }
+    // k-column register queue: a ring array whose column the body reads in its
+    // top plane and in at least one lower plane — the lower planes' values were
+    // read as the top plane of earlier steps and stay in registers
+    static constexpr bool queued(int a, int form) {
+        if (!P::on_ring(a) || P::span(a) < 2 || NS::is_int(a)) return false;
+        const int mp = P::march_pos(a);
+        if (!column(a, NS::ld_hi(a, mp), form)) return false;
+        for (int dz = NS::ld_lo(a, mp); dz < NS::ld_hi(a, mp); ++dz)
+            if (column(a, dz, form)) return true;
+        return false;
+    }
+};
+
+template <class MM, class FS, class NS, class P, int FORM, int PX, int PY, int PI, int NPTS>
+struct FastPt {
+    const MM& m;
+    const FS& fs;
+    typename MM::value_t (*q)[NPTS][P::maxspan() > 0 ? P::maxspan() : 1];   // [array][point][plane] queue
+    bool act;                                                                // the point is in the domain
+    template <int ARR>
+    using elem_t = typename MM::template elem_t<ARR>;
+
+    template <int ARR, int... O>
+    static constexpr int box_const() {   // element offset of this load relative to the thread's first point
+        constexpr int off[sizeof...(O)] = {O...};
+        int c = 0;
+        for (int p = 0; p < (int)sizeof...(O); ++p) {
+            const int s = NS::ld_sig(ARR, p);
+            if (s == 0) continue;
+            if (s == P::X) c += (off[p] + PX) * P::bstride(ARR, p);
+            else if (s == P::Y) c += (off[p] + PY) * P::bstride(ARR, p);
+            else c += (off[p] - P::lo(ARR, p)) * P::bstride(ARR, p);
+        }
+        return c;
+    }
+    template <int ARR, int... O>
+    static constexpr int plane_of() {
+        constexpr int off[sizeof...(O)] = {O...};
+        for (int p = 0; p < (int)sizeof...(O); ++p)
+            if (NS::ld_sig(ARR, p) == 0) return off[p] - NS::ld_lo(ARR, p);
+        return 0;
+    }
+    template <int ARR, int... O>
+    __device__ __forceinline__ long long gconst() const {   // global element offset (runtime strides)
+        constexpr int off[sizeof...(O)] = {O...};
+        long long c = 0;
+#pragma unroll
+        for (int p = 0; p < (int)sizeof...(O); ++p) {
+            const int s = NS::sig(ARR, p);
+            const int o = off[p] + (s == P::X ? PX : (s == P::Y ? PY : 0));
+            if (o != 0) c += (long long)o * m.g.a.arr[ARR].stride[p];
+        }
+        return c;
+    }
+
+    template <int ARR, int... O>
+    static constexpr bool at_column() {
+        constexpr int off[sizeof...(O)] = {O...};
+        for (int p = 0; p < (int)sizeof...(O); ++p)
+            if (NS::ld_sig(ARR, p) != 0 && off[p] != 0) return false;
+        return true;
+    }
+
+    template <int ARR, int... O>
+    __device__ __forceinline__ elem_t<ARR> ld() const {
+        if constexpr (FS::queued(ARR, FORM) && at_column<ARR, O...>()) {
+            constexpr int i = plane_of<ARR, O...>();
+            if constexpr (i < P::span(ARR) - 1) {
+                return q[ARR][PI][i];                    // read as the top plane of an earlier step
+            } else {
+                const elem_t<ARR> v = *reinterpret_cast<const elem_t<ARR>*>(
+                    m.ring + fs.plane[ARR][i] + box_const<ARR, O...>() * (int)sizeof(elem_t<ARR>));
+                q[ARR][PI][i] = v;
+                return v;
+            }
+        } else if constexpr (P::staged(ARR)) {
+            constexpr int c = box_const<ARR, O...>() * (int)sizeof(elem_t<ARR>);
+            const unsigned b = P::on_ring(ARR) ? fs.plane[ARR][plane_of<ARR, O...>()] : fs.stat[ARR];
+            return *reinterpret_cast<const elem_t<ARR>*>(m.ring + b + c);
+        } else if constexpr (FS::needs_gp(ARR, FORM)) {
+            const elem_t<ARR>* p = reinterpret_cast<const elem_t<ARR>*>(fs.gp[ARR]) + gconst<ARR, O...>();
+            if constexpr (NS::readonly(ARR)) return ld_ro(p);
+            else return ld_plain(p);
+        } else {
+            return m.template ld<ARR, O...>();
+        }
+    }
+    template <int ARR, class... I>
+    __device__ __forceinline__ elem_t<ARR> ldx(I... ii) const { return m.template ldx<ARR>(ii...); }
+    template <int ARR, class... I>
+    __device__ __forceinline__ elem_t<ARR> ldx_in(I... ii) const { return m.template ldx_in<ARR>(ii...); }
+    template <int ARR, int... O>
+    __device__ __forceinline__ void st(elem_t<ARR> v) const {
+        if (!act) return;
+        if constexpr (FS::stored_static(ARR, FORM)) {
+            if (!m.g.a.sh.enabled) {
+                *(reinterpret_cast<elem_t<ARR>*>(fs.gp[ARR]) + gconst<ARR, O...>()) = v;
+                return;
+            }
+        }
+        m.template st<ARR, O...>(v);   // sharded launch: write-through path
+    }
+    template <int ARR, class... A>
+    __device__ __forceinline__ void stx(A... args) const { m.template stx<ARR>(args...); }
+};
+
+// a thread's points: NPX along x strided by the block width (coalesced rows),
+// NPY ADJACENT rows (their shared y-neighbour rows are one LDS each)
+template <class NS, class P, class MM, class FS, int FORM, int NPX, int NPY, int BX, int I, class Q>
+__device__ __forceinline__ void fast_points(MM& m, const FS& fs, Q q, const KernelArgs<NS>& args, int* pt,
+                                            const bool* inb, int x0, int y0, int lx0, int ly0) {
+    if constexpr (I < NPX * NPY) {
+        constexpr int rx = I % NPX, ry = I / NPX;
+        if (FS::all_staged() || inb[I]) {
+            pt[P::X] = x0 + rx * BX;
+            if constexpr (NS::NLOOP == 3) pt[1] = y0 + ry;
+            if constexpr (NS::has_dynamic_index) {
+                m.lx = lx0 + rx * BX;
+                m.ly = ly0 + ry;
+            }
+            FastPt<MM, FS, NS, P, FORM, rx * BX, ry, I, NPX * NPY> fp{m, fs, q, inb[I]};
+            NS::template body<FORM>(fp, args.s, pt);
+        }
+        fast_points<NS, P, MM, FS, FORM, NPX, NPY, BX, I + 1>(m, fs, q, args, pt, inb, x0, y0, lx0, ly0);
+    }
+}
+
+// prologue of the k-column queue: the lower planes of step 0 from the ring
+template <class NS, class P, class FS, int FORM, int NPX, int NPY, int BX, int A, class T, class Q>
+__device__ __forceinline__ void fast_queue_fill(const unsigned char* ring, const FS& fs, Q q) {
+    if constexpr (A < NS::NARR) {
+        if constexpr (FS::queued(A, FORM)) {
+            constexpr int mp = P::march_pos(A);
+            int xo = 0;   // box element offset of the column (0, 0) relative to the thread's first point
+#pragma unroll
+            for (int p = 0; p < NS::ndim(A); ++p)
+                if (p != mp && NS::ld_sig(A, p) != P::X && NS::ld_sig(A, p) != P::Y)
+                    xo += (0 - P::lo(A, p)) * P::bstride(A, p);
+#pragma unroll
+            for (int I = 0; I < NPX * NPY; ++I) {
+                const int rx = I % NPX, ry = I / NPX;
+                int c = xo;
+#pragma unroll
+                for (int p = 0; p < NS::ndim(A); ++p) {
+                    if (NS::ld_sig(A, p) == P::X) c += rx * BX * P::bstride(A, p);
+                    else if (NS::ld_sig(A, p) == P::Y) c += ry * P::bstride(A, p);
+                }
+#pragma unroll
+                for (int i = 0; i < P::span(A) - 1; ++i)
+                    q[A][I][i] = *reinterpret_cast<const T*>(ring + fs.plane[A][i] + c * (int)sizeof(T));
+            }
+        }
+        fast_queue_fill<NS, P, FS, FORM, NPX, NPY, BX, A + 1, T>(ring, fs, q);
+    }
+}
+
+// end of step: the queue moves one plane along the march
+template <class NS, class P, class FS, int FORM, int NPTS, int A, class Q>
+__device__ __forceinline__ void fast_queue_shift(Q q) {
+    if constexpr (A < NS::NARR) {
+        if constexpr (FS::queued(A, FORM)) {
+#pragma unroll
+            for (int I = 0; I < NPTS; ++I)
+#pragma unroll
+                for (int i = 0; i + 1 < P::span(A); ++i) q[A][I][i] = q[A][I][i + 1];
+        }
+        fast_queue_shift<NS, P, FS, FORM, NPTS, A + 1>(q);
+    }
+}
+
 // TX x TY points per tile, BX x BY threads: each thread computes (TX/BX) x (TY/BY)
 // points per march step, amortising the step's barrier / mbarrier wait.
 template <class WP, class MM, class NS, int FORM, int RY, int R0, int RX>
@@ -742,6 +963,114 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
     }
 
     T win[WP::usable() ? WP::total() : 1];   // register windows, carried across steps (queue)
+    // RX == 1: the thread's per-array box offsets, global pointers and in-domain points (march-invariant)
+    // hoisted-addressing path (3-D nests, one point per thread column); 2-D row
+    // strips are DRAM-bound already and keep the generic path (smaller code)
+    constexpr bool FAST = RX == 1 && NS::NLOOP == 3;
+    using FS = FastState<NS, T, P, MS>;
+    constexpr int NPX = TX / BX, NPY = TY / BY, NPTS = NPX * NPY;
+    FS fs;
+    unsigned toff[NS::NARR];
+    bool inb[NPTS];
+    T q[NS::NARR][NPTS][MS > 0 ? MS : 1];          // k-column queues (queued arrays only; the rest is dead)
+    const int ly0 = ty * NPY;                       // the thread's first row (rows ly0 .. ly0 + NPY - 1)
+    auto set_planes = [&](int newest) {
+#pragma unroll
+        for (int a = 0; a < NS::NARR; ++a) {
+            if (!P::on_ring(a)) continue;
+            const int mp = P::march_pos(a);
+#pragma unroll
+            for (int i = 0; i < MS; ++i) {
+                if (i >= P::span(a)) continue;
+                int slot = newest + D + NS::ld_lo(a, mp) + i - NS::ld_hi(a, mp);
+                slot = slot >= D ? slot - D : slot;
+                fs.plane[a][i] = (unsigned)(slot * P::slot_bytes() + P::ring_off(a)) + toff[a];
+            }
+        }
+    };
+    if constexpr (FAST) {
+#pragma unroll
+        for (int a = 0; a < NS::NARR; ++a) {
+            toff[a] = 0;
+            fs.gp[a] = nullptr;
+            fs.gstep[a] = 0;
+            if (P::staged(a)) {
+                int e = 0;
+#pragma unroll
+                for (int p = 0; p < NS::ndim(a); ++p) {
+                    const int sg = NS::ld_sig(a, p);
+                    if (sg == P::X) e += (tx + m.sh[a] - P::lo(a, p)) * P::bstride(a, p);
+                    else if (sg == P::Y) e += (ly0 - P::lo(a, p)) * P::bstride(a, p);
+                }
+                toff[a] = (unsigned)(e * (int)P::esize(a));
+                if (P::is_static(a)) fs.stat[a] = (unsigned)(stat - ring) + (unsigned)P::static_off(a) + toff[a];
+            }
+            if (FS::needs_gp(a, FORM)) {
+                long long e = 0, st = 0;
+#pragma unroll
+                for (int p = 0; p < NS::ndim(a); ++p) {
+                    const int sg = NS::sig(a, p);
+                    const long long sd = args.arr[a].stride[p];
+                    if (sg == 0) {
+                        e += (long long)kb * sd;
+                        st += sd;
+                    } else if (sg == P::X) e += (long long)(orgx + tx) * sd;
+                    else if (NS::NLOOP == 3 && sg == 1) e += (long long)(orgy + ly0) * sd;
+                }
+                const int es = NS::is_int(a) ? 4 : (int)sizeof(T);
+                fs.gp[a] = static_cast<char*>(args.arr[a].base) + e * es;
+                fs.gstep[a] = st * es;
+            }
+        }
+#pragma unroll
+        for (int ry = 0; ry < NPY; ++ry)
+#pragma unroll
+            for (int rx = 0; rx < NPX; ++rx) {
+                const int x = orgx + tx + rx * BX, y = orgy + ly0 + ry;
+                inb[ry * NPX + rx] = x < args.hi[P::X] && x >= xlo0 && (NS::NLOOP < 3 || y < args.hi[1]);
+            }
+        if (ns > 0) {                               // step 0's lower planes are in (waited above)
+            set_planes((MS - 1) % D);
+            fast_queue_fill<NS, P, FS, FORM, NPX, NPY, BX, 0, T>(ring, fs, q);
+        }
+    }
+    if constexpr (FAST) {
+        // ring bookkeeping carried across steps (no division per step)
+        int newest = (MS - 1) % D, phase = ((MS - 1) / D) & 1, islot = (D - 1) % D;
+        auto step = [&](int s) __attribute__((always_inline)) {
+            __syncthreads();   // every thread is done with step s-1: its oldest slot is free
+            if (tid == 0 && s + D - 1 < nb) {
+                fence_proxy_async();
+                mbar_expect_tx(&bars[islot], P::slot_tx());
+                march_issue<P, NS, 0>(ring + islot * P::slot_bytes(), maps, &bars[islot], kb + s + D - 1 - (MS - 1),
+                                      orgx + maps.adjx, orgy, false, stat);
+            }
+            mbar_wait(&bars[newest], (uint32_t)phase);
+            pt[0] = kb + s;
+            m.k = kb + s;
+            m.newest = newest;
+            // this step's ring planes: one add per (array, plane) for all of the thread's points
+            set_planes(newest);
+            fast_points<NS, P, M, FS, FORM, NPX, NPY, BX, 0>(m, fs, q, args, pt, inb, orgx + tx, orgy + ly0, tx, ly0);
+            fast_queue_shift<NS, P, FS, FORM, NPTS, 0>(q);
+#pragma unroll
+            for (int a = 0; a < NS::NARR; ++a)
+                if (FS::needs_gp(a, FORM)) fs.gp[a] += fs.gstep[a];
+            islot = islot + 1 == D ? 0 : islot + 1;
+            if (++newest == D) {
+                newest = 0;
+                phase ^= 1;
+            }
+        };
+        // unrolled by the march span: the k-column queue shifts become register renames
+        constexpr int U = MS > 1 ? MS : 1;
+        int s = 0;
+        for (; s + U <= ns; s += U) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) step(s + u);
+        }
+        for (; s < ns; ++s) step(s);
+    } else {
     for (int s = 0; s < ns; ++s) {
         __syncthreads();   // every thread is done with step s-1: its oldest slot is free
         if (tid == 0) {
@@ -766,20 +1095,23 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
                 continue;
             }
         }
+        {
 #pragma unroll
-        for (int ry = 0; ry < TY / BY; ++ry) {
+            for (int ry = 0; ry < TY / BY; ++ry) {
 #pragma unroll
-            for (int rx = 0; rx < TX / BX; ++rx) {
-                m.lx = RX > 1 ? tx * RX + rx : tx + rx * BX;
-                m.ly = ty + ry * BY;
-                const int x = orgx + m.lx, y = orgy + m.ly;
-                if (x < args.hi[P::X] && x >= xlo0 && (NS::NLOOP < 3 || y < args.hi[1])) {
-                    pt[P::X] = x;
-                    if constexpr (NS::NLOOP == 3) pt[1] = y;
-                    NS::template body<FORM>(m, args.s, pt);
+                for (int rx = 0; rx < TX / BX; ++rx) {
+                    m.lx = RX > 1 ? tx * RX + rx : tx + rx * BX;
+                    m.ly = ty + ry * BY;
+                    const int x = orgx + m.lx, y = orgy + m.ly;
+                    if (x < args.hi[P::X] && x >= xlo0 && (NS::NLOOP < 3 || y < args.hi[1])) {
+                        pt[P::X] = x;
+                        if constexpr (NS::NLOOP == 3) pt[1] = y;
+                        NS::template body<FORM>(m, args.s, pt);
+                    }
                 }
             }
         }
+    }
     }
     if (args.sh.enabled) __threadfence_system();   // peer write-through visible before the step flag
 }

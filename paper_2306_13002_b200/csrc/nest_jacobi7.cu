@@ -13,13 +13,13 @@ void register_jacobi7() {
         describe<gen::jacobi7>(e, "jacobi7.c", 0);
         e.row_offset = true;   // sector-aligned rows; the TMA maps start adj elements earlier
         fill_naive<gen::jacobi7, double>(e, 0);
-        fill_march<gen::jacobi7, double, 0, 64, 4, 64, 4, 3>(e, 0);
-        fill_march<gen::jacobi7, double, 0, 128, 4, 128, 2, 5>(e, 0);
-        fill_march<gen::jacobi7, double, 0, 32, 16, 32, 4, 3>(e, 0);
+        fill_march<gen::jacobi7, double, 0, 128, 8, 128, 2, 2>(e, 0);
+        fill_march<gen::jacobi7, double, 0, 128, 8, 128, 2, 3>(e, 0);
+        fill_march<gen::jacobi7, double, 0, 128, 8, 128, 4, 3>(e, 0);
         fill_march<gen::jacobi7, double, 0, 128, 4, 128, 2, 2>(e, 0);
-        fill_march<gen::jacobi7, double, 0, 128, 4, 128, 2, 4>(e, 0);
+        fill_march<gen::jacobi7, double, 0, 128, 16, 128, 4, 2>(e, 0);
         fill_march<gen::jacobi7, double, 0, 128, 4, 128, 2, 3>(e, 0);
-        fill_march<gen::jacobi7, double, 0, 128, 8, 64, 4, 2, 2>(e, 0);
+        fill_march<gen::jacobi7, double, 0, 128, 16, 64, 4, 2, 2>(e, 0);
         register_entry(&e);
     }
 }
