@@ -190,7 +190,10 @@ acs_status acs_tune(const acs_kernel* k, acs_variant variant, const acs_array* a
  * g >= own_hi - halo (peer device memory: NVLink P2P, or the same device).
  * `halo` is how far beyond its owned range the NEXT step reads the produced
  * data (wave4: 2, jacobi7: 1, D3Q19 push-stream: 0 — only pushes into the
- * neighbour's planes travel).  Order steps across ranks with acs_signal /
+ * neighbour's planes travel; swim / CloverLeaf multi-kernel steps: 1).  No
+ * store is forwarded below the upper neighbour's `hi_origin` (its first
+ * buffer plane), so slabs whose stores reach past the owned range (swim's
+ * j+1 stores) stay inside the neighbour's buffer.  Order steps across ranks with acs_signal /
  * acs_wait (device-side release/acquire flags, no host round trip).
  * Neighbours' buffers must have the same element strides as this rank's
  * (allocate every slab with the same plane count; use views for the rest). */
@@ -225,6 +228,12 @@ acs_status acs_wait(const uint64_t* flag_a, const uint64_t* flag_b, uint64_t val
 acs_status acs_signal_ctr(uint64_t* flag_a, uint64_t* flag_b, uint64_t* counter, void* cuda_stream);
 acs_status acs_wait_ctr(const uint64_t* flag_a, const uint64_t* flag_b, const uint64_t* counter, int timeout_ms,
                         void* cuda_stream);
+/* Loads the code of every schedule slot of (kernel, variant) for these arrays
+ * without launching anything.  CUDA lazy loading loads a kernel at its first
+ * launch and may wait for the device to drain: call this before a sharded
+ * time loop whose acs_wait_ctr kernels spin while other streams launch. */
+acs_status acs_preload(const acs_kernel* k, acs_variant variant, const acs_array* arrays, int n_arrays,
+                       const acs_scalar* scalars, int n_scalars);
 /* CUDA IPC of a device pointer inside any allocation (base handle + offset) */
 acs_status acs_ipc_export(const void* dptr, void* handle_out /* 64 bytes */, int64_t* offset_out);
 acs_status acs_ipc_import(const void* handle /* 64 bytes */, int64_t offset, void** dptr_out);

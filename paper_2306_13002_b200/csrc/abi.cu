@@ -479,6 +479,29 @@ acs_status acs_wait(const uint64_t* flag_a, const uint64_t* flag_b, uint64_t val
     return check_launch("acs_wait");
 }
 
+acs_status acs_preload(const acs_kernel* k, acs_variant variant, const acs_array* arrays, int n_arrays,
+                       const acs_scalar* scalars, int n_scalars) {
+    if (!k || (int)variant < 0 || (int)variant > 5) {
+        set_error("acs_preload: bad argument");
+        return ACS_E_ARG;
+    }
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    const int prec = precision_of(arrays, n_arrays);
+    LaunchReq r{arrays, n_arrays, scalars, n_scalars, nullptr, nullptr, false, true};
+    for (int slot = 0; slot < kMaxSched; ++slot) {
+        LaunchFn fn = e->launch[prec][variant][slot];
+        if (!fn) continue;
+        const acs_status st = fn(r);
+        if (st != ACS_OK && st != ACS_E_LAYOUT) return st;
+    }
+    // the step-ordering kernels too
+    if (preload_fn((const void*)wait_ctr_kernel) != ACS_OK || preload_fn((const void*)signal_ctr_kernel) != ACS_OK) {
+        set_error("acs_preload: cudaFuncGetAttributes failed");
+        return ACS_E_CUDA;
+    }
+    return ACS_OK;
+}
+
 acs_status acs_signal_ctr(uint64_t* flag_a, uint64_t* flag_b, uint64_t* counter, void* cuda_stream) {
     if (!counter) {
         set_error("acs_signal_ctr: null counter");

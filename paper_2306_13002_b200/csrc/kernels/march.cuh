@@ -1248,6 +1248,7 @@ acs_status launch_march(const LaunchReq& r) {
     if (kchunk > nz) kchunk = nz;
     const long long chunks = (nz + kchunk - 1) / kchunk;
     dim3 grid((unsigned)((nx + TX - 1) / TX), (unsigned)(NL == 3 ? (ny + TY - 1) / TY : 1), (unsigned)chunks);
+    if (r.preload) return preload_fn((const void*)kern);
     kern<<<grid, dim3(BX, BY, 1), smem, r.stream>>>(ka, maps, (int)kchunk);
     return check_launch("march");
 }

@@ -246,6 +246,7 @@ acs_status launch_sliced(const LaunchReq& r) {
     const long long nx = ka.hi[2] - x0, ny = ka.hi[1] - ka.lo[1], nz = ka.hi[0] - ka.lo[0];
     const long long chunks = (nz + KCH - 1) / KCH;
     dim3 grid((unsigned)((nx + BX - 1) / BX), (unsigned)((ny + BY - 1) / BY), (unsigned)(chunks * NSL));
+    if (r.preload) return preload_fn((const void*)sliced_kernel<NS, T, FORM, BX, BY, UNR>);
     sliced_kernel<NS, T, FORM, BX, BY, UNR><<<grid, dim3(BX, BY, 1), 0, r.stream>>>(ka, KCH);
     return check_launch("sliced");
 }

@@ -219,6 +219,7 @@ acs_status launch_stream(const LaunchReq& r) {
     if (rpc < 4) rpc = 4;
     if (rpc > nrows) rpc = nrows;
     dim3 grid((unsigned)xt, (unsigned)((nrows + rpc - 1) / rpc), 1);
+    if (r.preload) return preload_fn((const void*)kern);
     kern<<<grid, BX, smem, r.stream>>>(ka, (int)rpc);
     return check_launch("stream");
 }

@@ -29,7 +29,17 @@ struct LaunchReq {
     cudaStream_t stream;
     const acs_shard* shard = nullptr;   // slab-sharded launch (acs_launch_sharded)
     bool strict = false;   // explicit slot: a skeleton that cannot take the layout fails (ACS_E_LAYOUT)
+    bool preload = false;  // load the kernel's code (acs_preload) instead of launching it
 };
+
+// CUDA lazy loading loads a kernel's code at its first launch and may wait for
+// the device to drain first: a kernel first launched while another stream's
+// acs_wait_ctr spins on a neighbour would deadlock.  acs_preload loads every
+// skeleton of a kernel up front.
+inline acs_status preload_fn(const void* kern) {
+    cudaFuncAttributes a;
+    return cudaFuncGetAttributes(&a, kern) == cudaSuccess ? ACS_OK : ACS_E_CUDA;
+}
 
 using LaunchFn = acs_status (*)(const LaunchReq&);
 
@@ -150,6 +160,10 @@ acs_status bind(const LaunchReq& r, KernelArgs<NS>& ka, bool& empty) {
         ka.sh.origin = sd.origin;
         ka.sh.lo_thr = sd.own_lo + sd.halo;
         ka.sh.hi_thr = sd.own_hi - sd.halo;
+        // never forward below the upper neighbour's first buffer plane (a slab
+        // whose stores reach past its owned range but whose reads do not look
+        // back, e.g. swim's j+1 stores with no j-1 halo)
+        if (sd.hi_origin > ka.sh.hi_thr) ka.sh.hi_thr = sd.hi_origin;
         for (int i = 0; i < sd.n_sharded; ++i) {
             int a = -1;
             for (int b = 0; b < NS::NARR; ++b)
@@ -234,6 +248,7 @@ acs_status launch_naive(const LaunchReq& r) {
     }
     // ORIGINAL keeps every as-written load and store (ld_asis); the emitted
     // forms use ordinary (read-only-path where legal) accesses.
+    if (r.preload) return preload_fn((const void*)naive_kernel<NS, T, FORM, FORM == ACS_ORIGINAL, MINB>);
     naive_kernel<NS, T, FORM, FORM == ACS_ORIGINAL, MINB><<<grid, block, 0, r.stream>>>(ka);
     return check_launch(NS::array_names[0]);
 }
@@ -253,6 +268,7 @@ acs_status launch_naive_multi(const LaunchReq& r) {
     dim3 block(bx, by, 1);
     dim3 grid((unsigned)((nx + (long long)bx * R - 1) / ((long long)bx * R)), (unsigned)((ny + by - 1) / by),
               NL >= 3 ? (unsigned)(ka.hi[0] - ka.lo[0]) : 1u);
+    if (r.preload) return preload_fn((const void*)naive_multi_kernel<NS, T, FORM, R>);
     naive_multi_kernel<NS, T, FORM, R><<<grid, block, 0, r.stream>>>(ka);
     return check_launch(NS::array_names[0]);
 }

@@ -342,3 +342,16 @@ def rotation_period(nest: str) -> int:
         p = p * len(group) // np.gcd(p, len(group))
     return p
 
+
+def pipeline_inputs(kernel_ids, size=None, dtype: str = "f64"):
+    """Host inputs of a multi-kernel step (shard.PIPELINES): the union of the
+    kernels' arrays, each filled by the first kernel that declares it (the
+    same rule SlabRank uses on the device).  Returns (arrays, workloads)."""
+    ws = [workload(k, size, dtype=dtype) for k in kernel_ids]
+    out: Dict[str, np.ndarray] = {}
+    for w in ws:
+        ins = make_inputs(w)
+        for p in w.spec.arrays:
+            out.setdefault(p.name, ins[p.name])
+    return out, ws
+

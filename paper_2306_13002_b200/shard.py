@@ -79,7 +79,12 @@ def plan_for(w: nests.Workload, nranks: int) -> SlabPlan:
     first = next(a for a in w.spec.arrays if len(w.dims[a.name]) >= 2)
     dim0 = w.dims[first.name][0]
     reach_lo, reach_hi = glo, dim0 - ghi
+    # halo: rows within `halo` of a slab face are written through to the
+    # neighbour (never below the upper neighbour's first buffer row); it must
+    # not exceed reach_hi (the lower neighbour's window ends reach_hi rows above
+    # its owned range)
     halo = {"jacobi7": 1, "wave4": 2, "d3q19": 0, "swim": 1, "clover": 1}[w.spec.nest]
+    assert halo <= reach_hi, (w.spec.kernel_id, halo, reach_hi)
     # neighbours exchange only with ranks +-1: every slab must own at least
     # the planes the next step reads across its face (and one plane at all)
     need = max(1, halo, reach_lo, reach_hi)
@@ -126,6 +131,9 @@ def _fns():
         L.acs_signal_ctr.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.acs_wait_ctr.restype = ctypes.c_int
         L.acs_wait_ctr.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+        L.acs_preload.restype = ctypes.c_int
+        L.acs_preload.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(backend.AcsArray), ctypes.c_int,
+                                  ctypes.POINTER(backend.AcsScalar), ctypes.c_int]
         L.acs_ipc_export.restype = ctypes.c_int
         L.acs_ipc_export.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]
         L.acs_ipc_import.restype = ctypes.c_int
@@ -166,11 +174,37 @@ def plane_view(t, lo: int, hi: int):
     return torch.as_strided(t, (n,), (1,), t.storage_offset() + lo * st[0])
 
 
+def written_rows(own: Tuple[int, int], st_lo: int, st_hi: int) -> Tuple[int, int]:
+    """Global rows [lo, hi) a rank owning outer-loop range `own` writes into an
+    array whose stores reach subscript-0 offsets [st_lo, st_hi]."""
+    return own[0] + st_lo, own[1] + st_hi
+
+
+def exchange_rows(plan: SlabPlan, rank: int, st_lo: int, st_hi: int):
+    """Row exchange of one produced array after a kernel, in GLOBAL rows:
+    (peer, send rows, recv rows).  A rank sends every row it wrote that lies in
+    the neighbour's buffer window and receives every row the neighbour wrote
+    that lies in its own — owner computes writes each element exactly once,
+    so with row-disjoint stores (store reach of one row) nothing received
+    overwrites a row the receiver wrote itself."""
+    out = []
+    me = written_rows(plan.owned(rank), st_lo, st_hi)
+    win = lambda r: (plan.origin(r), plan.origin(r) + plan.local_planes(r))   # noqa: E731
+    for peer in (rank - 1, rank + 1):
+        if peer < 0 or peer >= plan.nranks:
+            continue
+        theirs = written_rows(plan.owned(peer), st_lo, st_hi)
+        pw, mw = win(peer), win(rank)
+        send = (max(me[0], pw[0]), min(me[1], pw[1]))
+        recv = (max(theirs[0], mw[0]), min(theirs[1], mw[1]))
+        out.append((peer, send, recv))
+    return out
+
+
 def exchange_ops(rank: int, nranks: int, lo: int, hi: int, halo: int):
-    """The halo exchange of one produced array after a step, in LOCAL plane
-    coordinates of a rank owning [lo, hi): (peer, send planes, recv planes).
-    The lower neighbour gets this rank's first `halo` owned planes and sends
-    its last ones into [lo - halo, lo); symmetrically for the upper one."""
+    """The halo exchange of a produced array whose stores stay on the point's
+    own plane, in LOCAL plane coordinates of a rank owning [lo, hi) with a
+    `halo`-plane read halo: (peer, send planes, recv planes)."""
     out = []
     if halo <= 0:
         return out
@@ -181,57 +215,90 @@ def exchange_ops(rank: int, nranks: int, lo: int, hi: int, halo: int):
     return out
 
 
-def halo_exchange(dist, rank: int, nranks: int, t, lo: int, hi: int, halo: int, group=None) -> None:
-    """Sends / receives the boundary planes of `t` with ranks +-1 through
-    torch.distributed P2P (batched: one NCCL group on GPUs).  Enqueued on
-    the CURRENT stream; returns once the receives are ordered before later
-    work on that stream."""
-    ops = []
-    for peer, (slo, shi), (rlo, rhi) in exchange_ops(rank, nranks, lo, hi, halo):
-        ops.append(dist.P2POp(dist.isend, plane_view(t, slo, shi), peer, group))
-        ops.append(dist.P2POp(dist.irecv, plane_view(t, rlo, rhi), peer, group))
-    if ops:
-        for w in dist.batch_isend_irecv(ops):
+def p2p_exchange(dist, t, ops, group=None) -> None:
+    """Posts (peer, (send lo, hi), (recv lo, hi)) plane exchanges of `t` as one
+    batch of torch.distributed P2P ops (one NCCL group on GPUs) on the CURRENT
+    stream and orders later work on that stream after the receives."""
+    p2p = []
+    for peer, (slo, shi), (rlo, rhi) in ops:
+        if shi > slo:
+            p2p.append(dist.P2POp(dist.isend, plane_view(t, slo, shi), peer, group))
+        if rhi > rlo:
+            p2p.append(dist.P2POp(dist.irecv, plane_view(t, rlo, rhi), peer, group))
+    if p2p:
+        for w in dist.batch_isend_irecv(p2p):
             w.wait()
 
 
-class SlabRank:
-    """One rank's slab of a nest: local buffers, neighbour pointers, step loop.
+def halo_exchange(dist, rank: int, nranks: int, t, lo: int, hi: int, halo: int, group=None) -> None:
+    """Sends / receives the boundary planes of `t` with ranks +-1 (exchange_ops)."""
+    p2p_exchange(dist, t, exchange_ops(rank, nranks, lo, hi, halo), group)
 
-    Two data paths for the per-step neighbour exchange:
+
+# multi-kernel steps: a benchmark time step of the 2-D nests is a sequence of
+# registered regions over the same arrays (SPEC swim: calc1 -> calc2 -> calc3,
+# the last copying the new fields back; CloverLeaf: ideal_gas -> PdV ->
+# advec_cell x), every kernel over the rank's owned rows
+PIPELINES = {
+    "swim": ["swim.c:calc1:0", "swim.c:calc2:1", "swim.c:calc3:2"],
+    "clover": ["clover.c:ideal_gas:0", "clover.c:pdv_predict:1", "clover.c:advec_cell_x:2"],
+}
+
+
+class SlabRank:
+    """One rank's slab of a nest (or of a multi-kernel step): local buffers,
+    neighbour pointers, step loop.
+
+    `kernel_id` is one registered region (its time loop rotates buffers per
+    nests.ROTATIONS) or a list of regions run in order as one step over the
+    union of their arrays (PIPELINES).  Two data paths for the neighbour
+    exchange after every kernel:
 
     * **peer memory** (``connect_local`` / ``connect_ipc``): neighbour buffers
       are raw device pointers (same process, or CUDA-IPC imports over
       NVLink); the compute kernel writes boundary stores through to them and
-      device flags order the steps (``acs_wait_ctr`` / ``acs_signal_ctr``).
-      A step is (wait, launch, signal) with the step number in a device
-      counter, so it is captured once per rotation phase as a CUDA graph
-      (``capture``) and replayed: no host work per step.
+      device flags order the kernels (``acs_wait_ctr`` / ``acs_signal_ctr``).
+      A step is (wait, launch, signal) per kernel with the step count in a
+      device counter, so it is captured once per rotation phase as a CUDA
+      graph (``capture``) and replayed: no host work per step.
     * **message passing** (``connect_p2p``, NCCL over NVLink when peer
-      mapping is unavailable): the boundary planes are computed first, handed
-      to a communication stream that exchanges them with ``halo_exchange``
-      while the interior planes compute; the next step waits for the
-      exchange.  Halo-read nests only (jacobi7, wave4): D3Q19's push stream
-      writes into the neighbour's planes and needs peer memory."""
+      mapping is unavailable): single-kernel halo nests compute their boundary
+      planes first and exchange them on a communication stream while the
+      interior planes compute; multi-kernel steps exchange each kernel's
+      written rows (``exchange_rows``) before the next kernel.  Row-disjoint
+      stores only: D3Q19's push stream writes into rows its neighbours also
+      write and needs peer memory."""
 
-    def __init__(self, kernel_id: str, size, nranks: int, rank: int, dtype: str = "f64",
+    def __init__(self, kernel_id, size, nranks: int, rank: int, dtype: str = "f64",
                  variant: str = "accsat", schedule="default"):
         import torch
         self.torch = torch
-        self.k = backend.Kernel.lookup(kernel_id)
-        self.gw = nests.workload(kernel_id, size, dtype=dtype)
+        self.ids = [kernel_id] if isinstance(kernel_id, str) else list(kernel_id)
+        self.ks = [backend.Kernel.lookup(k) for k in self.ids]
+        self.gws = [nests.workload(k, size, dtype=dtype) for k in self.ids]
+        self.k, self.gw = self.ks[0], self.gws[0]
         self.plan = plan_for(self.gw, nranks)
         self.rank, self.nranks = rank, nranks
-        self.w = local_workload(self.gw, self.plan, rank)
-        self.variant, self.schedule = variant, schedule
+        self.ws = [local_workload(g, self.plan, rank) for g in self.gws]
+        self.w = self.ws[0]
+        self.variant = variant
+        self.schedule = schedule                      # one value, or one per kernel
         self.nest = self.gw.spec.nest
-        self.names = [a.name for a in self.w.spec.arrays]
-        self.sharded = [g for grp in ROTATIONS[self.nest] for g in grp]
-        self.period = nests.rotation_period(self.nest)
+        self.multi = len(self.ids) > 1
+        # union of the kernels' arrays (first appearance wins for dims and fill)
+        self.arrays: Dict[str, Tuple[nests.ParamSpec, nests.Workload]] = {}
+        for lw in self.ws:
+            for p in lw.spec.arrays:
+                self.arrays.setdefault(p.name, (p, lw))
+        self.names = list(self.arrays)
+        written = [n for lw in self.ws for n in lw.write_arrays]
+        self.sharded = (list(dict.fromkeys(written)) if self.multi
+                        else [g for grp in ROTATIONS[self.nest] for g in grp])
+        self.period = 1 if self.multi else nests.rotation_period(self.nest)
         self.step_no = 0
         self.buf = self._alloc()
         # [from lower, from upper] step flags (neighbours store into them), and
-        # this rank's completed-step counter
+        # this rank's completed-kernel counter
         self.flags = torch.zeros(2, dtype=torch.int64, device="cuda")
         self.ctr = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.lo_ptr: Dict[str, int] = {}
@@ -244,6 +311,31 @@ class SlabRank:
         self.comm_stream = None
         self.comm_done = None
         self.graphs = None
+        self._reach = None
+        self.preload()
+
+    def preload(self) -> None:
+        """acs_preload for every kernel of the step (see include/accsat_b200.h):
+        no kernel code may load lazily while a neighbour's wait kernel spins."""
+        L = _fns()
+        for ki, (k, lw) in enumerate(zip(self.ks, self.ws)):
+            names = [a.name for a in lw.spec.arrays]
+            descs, sc = k._pack({n: self.buf[n] for n in names}, dict(lw.scalars))
+            backend._check(L.acs_preload(k.handle, backend.VARIANTS[self.variant], descs, len(names), sc,
+                                         len(lw.scalars)), f"acs_preload({k.kernel_id})")
+
+    @property
+    def points(self) -> int:
+        return self.w.points
+
+    @property
+    def algorithmic_bytes(self) -> int:
+        """This rank's bytes per step (every kernel of the step)."""
+        return sum(lw.algorithmic_bytes for lw in self.ws)
+
+    @property
+    def global_bytes(self) -> int:
+        return sum(g.algorithmic_bytes for g in self.gws)
 
     def _alloc(self):
         """Local buffers, filled with the GLOBAL workload's values (flat offset
@@ -256,15 +348,16 @@ class SlabRank:
         # store to a neighbour at (its own index + a constant plane offset),
         # which must hold for the q-major D3Q19 layout too
         maxp = max(self.plan.local_planes(r) for r in range(self.nranks))
-        for p in self.w.spec.arrays:
-            dims = self.w.dims[p.name]
+        for name, (p, lw) in self.arrays.items():
+            dims = lw.dims[name]
             dt = torch.int32 if p.ctype == "int" else tdt
+            k = next(kk for kk, w in zip(self.ks, self.ws) if name in [a.name for a in w.spec.arrays])
             if len(dims) >= 2:
-                full = backend.empty_native(self.k, p.name, (maxp,) + tuple(dims[1:]), dt)
+                full = backend.empty_native(k, name, (maxp,) + tuple(dims[1:]), dt)
                 t = full[:dims[0]]
             else:
-                t = backend.empty_native(self.k, p.name, dims, dt)
-            out[p.name] = t
+                t = backend.empty_native(k, name, dims, dt)
+            out[name] = t
         self.refill(out)
         return out
 
@@ -276,11 +369,11 @@ class SlabRank:
         step."""
         bufs = self.buf if bufs is None else bufs
         origin = self.plan.origin(self.rank)
-        for p in self.w.spec.arrays:
-            t = bufs[p.name]
-            dims = self.w.dims[p.name]
+        for name, (p, lw) in self.arrays.items():
+            t = bufs[name]
+            dims = lw.dims[name]
             plane = int(np.prod(dims[1:])) if len(dims) > 1 else 0
-            fl = self.w.fills[p.name]
+            fl = lw.fills[name]
             off = origin * plane if len(dims) > 1 else 0
             if fl.kind == "copy":
                 backend.copy(t, bufs[fl.src])
@@ -336,11 +429,23 @@ class SlabRank:
         self.mode = "peer" if (lower is not None or upper is not None) else "none"
         self.graphs = None
 
+    def reach(self, ki: int) -> Dict[str, "object"]:
+        if self._reach is None:
+            from . import pipeline_exec
+            self._reach = [pipeline_exec.reaches(k) for k in self.ks]
+        return self._reach[ki]
+
     def connect_p2p(self, dist, group=None) -> None:
         """Message-passing exchange through torch.distributed (NCCL)."""
-        if self.plan.halo <= 0:
-            raise NotImplementedError(f"{self.k.kernel_id}: the push-stream exchange writes into the neighbour's "
-                                      "planes; it needs peer memory (connect_ipc)")
+        for ki, lw in enumerate(self.ws):
+            for n in lw.write_arrays:
+                r = self.reach(ki)[n]
+                if r.sliced and r.st_hi != r.st_lo:
+                    raise NotImplementedError(
+                        f"{self.ids[ki]}: stores of '{n}' reach rows {r.st_lo}..{r.st_hi} around the point — rows "
+                        "its neighbours write too (push stream); it needs peer memory (connect_ipc)")
+        if not self.multi and self.plan.halo <= 0:
+            raise NotImplementedError(f"{self.k.kernel_id}: no halo to exchange; it needs peer memory")
         self.mode = "p2p" if self.nranks > 1 else "none"
         self.dist, self.group = dist, group
         self.comm_stream = self.torch.cuda.Stream()
@@ -355,41 +460,67 @@ class SlabRank:
         self.graphs = None
 
     # -- stepping
-    def _sched(self):
-        return 16 + self.schedule if isinstance(self.schedule, int) else backend.SCHEDULES[self.schedule]
+    def _sched(self, ki: int = 0):
+        sc = self.schedule[ki] if isinstance(self.schedule, (list, tuple)) else self.schedule
+        return 16 + sc if isinstance(sc, int) else backend.SCHEDULES[sc]
 
-    def _launch(self, s: int, h, scalars=None, write_through: bool = True) -> None:
+    def _launch(self, s: int, h, scalars=None, write_through: bool = True, ki: int = 0) -> None:
         L = _fns()
-        roles = role_buffers(self.nest, self.names, s)
+        lw, k = self.ws[ki], self.ks[ki]
+        names = [a.name for a in lw.spec.arrays]
+        roles = role_buffers(self.nest, names, s) if not self.multi else {n: n for n in names}
         arrays = {p: self.buf[b] for p, b in roles.items()}
-        descs, sc = self.k._pack(arrays, dict(scalars or self.w.scalars))
+        sc_in = dict(scalars or lw.scalars)
+        descs, sc = k._pack(arrays, sc_in)
         sd = AcsShard()
         lo, hi = self.plan.owned(self.rank)
         sd.own_lo, sd.own_hi, sd.origin, sd.halo = lo, hi, self.plan.origin(self.rank), self.plan.halo
-        names = [n for n in self.sharded if n in self.w.write_arrays] if write_through else []   # produced arrays
-        sd.n_sharded = len(names)
-        keep = [n.encode() for n in names]
-        for i, n in enumerate(names):
+        names_wt = [n for n in self.sharded if n in lw.write_arrays] if write_through else []   # produced arrays
+        sd.n_sharded = len(names_wt)
+        keep = [n.encode() for n in names_wt]
+        for i, n in enumerate(names_wt):
             sd.names[i] = keep[i]
             sd.lo_data[i] = self.lo_ptr.get(roles[n]) if self.lo_ptr else None
             sd.hi_data[i] = self.hi_ptr.get(roles[n]) if self.hi_ptr else None
         sd.lo_origin, sd.hi_origin = self.lo_origin, self.hi_origin
-        backend._check(L.acs_launch_sharded(self.k.handle, backend.VARIANTS[self.variant], self._sched(), descs,
-                                            len(arrays), sc, len(scalars or self.w.scalars), ctypes.byref(sd), h),
-                       f"acs_launch_sharded({self.k.kernel_id})")
+        backend._check(L.acs_launch_sharded(k.handle, backend.VARIANTS[self.variant], self._sched(ki), descs,
+                                            len(arrays), sc, len(sc_in), ctypes.byref(sd), h),
+                       f"acs_launch_sharded({k.kernel_id})")
 
     def _enqueue_peer(self, s: int, h, timeout_ms: int, before_launch=None) -> None:
         L = _fns()
         neighbours = bool(self.lo_ptr or self.hi_ptr)
-        if neighbours:
-            backend._check(L.acs_wait_ctr(self.flags.data_ptr() if self.lo_ptr else None,
-                                          self.flags.data_ptr() + 8 if self.hi_ptr else None,
-                                          self.ctr.data_ptr(), timeout_ms, h), "acs_wait_ctr")
+        for ki in range(len(self.ks)):
+            if neighbours:
+                backend._check(L.acs_wait_ctr(self.flags.data_ptr() if self.lo_ptr else None,
+                                              self.flags.data_ptr() + 8 if self.hi_ptr else None,
+                                              self.ctr.data_ptr(), timeout_ms, h), "acs_wait_ctr")
+            if before_launch is not None and ki == 0:
+                before_launch(s, h)
+            self._launch(s, h, ki=ki)
+            if neighbours:
+                backend._check(L.acs_signal_ctr(self.lo_flag, self.hi_flag, self.ctr.data_ptr(), h),
+                               "acs_signal_ctr")
+
+    def _step_p2p_multi(self, s: int, stream, before_launch=None) -> None:
+        """Every kernel over the owned rows, then its written rows exchanged
+        with the neighbours before the next kernel."""
+        torch = self.torch
+        stream = stream or torch.cuda.current_stream()
+        h = backend._stream_handle(stream)
         if before_launch is not None:
             before_launch(s, h)
-        self._launch(s, h)
-        if neighbours:
-            backend._check(L.acs_signal_ctr(self.lo_flag, self.hi_flag, self.ctr.data_ptr(), h), "acs_signal_ctr")
+        for ki, lw in enumerate(self.ws):
+            self._launch(s, h, write_through=False, ki=ki)
+            with torch.cuda.stream(stream):
+                for n in lw.write_arrays:
+                    r = self.reach(ki)[n]
+                    if not r.sliced:
+                        continue
+                    o = self.plan.origin(self.rank)
+                    ops = [(peer, (a - o, b - o), (c - o, d - o))
+                           for peer, (a, b), (c, d) in exchange_rows(self.plan, self.rank, r.st_lo, r.st_hi)]
+                    p2p_exchange(self.dist, self.buf[n], ops, self.group)
 
     def _step_p2p(self, s: int, stream, before_launch=None) -> None:
         """Boundary planes, then their exchange on the comm stream overlapped
@@ -430,7 +561,10 @@ class SlabRank:
         buffers."""
         s = self.step_no
         if self.mode == "p2p":
-            self._step_p2p(s, stream, before_launch)
+            if self.multi:
+                self._step_p2p_multi(s, stream, before_launch)
+            else:
+                self._step_p2p(s, stream, before_launch)
         elif self.graphs is not None and before_launch is None:
             with self.torch.cuda.stream(stream or self.torch.cuda.current_stream()):
                 self.graphs[s % self.period].replay()
@@ -440,8 +574,8 @@ class SlabRank:
 
     def capture(self, stream=None, timeout_ms: int = 20000) -> None:
         """Captures one CUDA graph per rotation phase of the peer-memory step
-        (wait_ctr, launch with write-through, signal_ctr); ``step`` then
-        replays them.  The device counter carries the step number."""
+        (per kernel: wait_ctr, launch with write-through, signal_ctr); ``step``
+        then replays them.  The device counter carries the step number."""
         if self.mode == "p2p":
             raise RuntimeError("capture: the message-passing step is not captured (NCCL P2P owns its streams)")
         torch = self.torch
@@ -459,8 +593,19 @@ class SlabRank:
         torch.cuda.synchronize()
         self.graphs = graphs
 
+    def launches_per_step(self) -> int:
+        """Kernels this rank enqueues per step (the bench's gpu_launches)."""
+        nk = len(self.ks)
+        if self.mode == "peer":
+            return 3 * nk
+        if self.mode == "p2p" and not self.multi:
+            return 1 + (self.rank > 0) + (self.rank < self.nranks - 1)
+        return nk
+
     def current(self, name: str):
         """Physical buffer holding parameter `name` after the steps so far."""
+        if self.multi:
+            return self.buf[name]
         return self.buf[role_buffers(self.nest, self.names, self.step_no)[name]]
 
     def owned_slice(self, name: str):

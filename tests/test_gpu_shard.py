@@ -303,3 +303,81 @@ def test_message_passing_rejects_push_stream():
     sr = shard.SlabRank("d3q19.c:stream_collide:0", (8, 5, 6), 2, 0)
     with pytest.raises(NotImplementedError):
         sr.connect_p2p(None)
+
+
+def single_pipeline(nest, size, steps):
+    ids = shard.PIPELINES[nest]
+    g, ws = nests.pipeline_inputs(ids, size)
+    for _ in range(steps):
+        for w in ws:
+            oracle_cpu.run(w.spec, {p.name: g[p.name] for p in w.spec.arrays}, w.scalars, "accsat", fma=True)
+    return g, ws
+
+
+@pytest.mark.parametrize("nest,size,nranks,sched", [("swim", (24, 70), 2, "tiled"), ("swim", (27, 37), 3, "naive"),
+                                                    ("clover", (22, 70), 2, "tiled"), ("clover", (25, 37), 3, "naive")])
+@pytest.mark.parametrize("graph", [False, True])
+def test_sharded_pipeline_peer(nest, size, nranks, sched, graph):
+    """Multi-kernel steps (swim calc1 -> calc2 -> calc3, CloverLeaf ideal_gas ->
+    PdV -> advec) slab-sharded with peer write-through after every kernel,
+    eager or graph-replayed: bit-exact vs the single domain."""
+    torch = _torch()
+    steps = 3
+    g, ws = single_pipeline(nest, size, steps)
+    ids = shard.PIPELINES[nest]
+    ranks = [shard.SlabRank(ids, size, nranks, r, schedule=sched) for r in range(nranks)]
+    for r, sr in enumerate(ranks):
+        sr.connect_local(ranks[r - 1] if r > 0 else None, ranks[r + 1] if r < nranks - 1 else None)
+    streams = [torch.cuda.Stream() for _ in ranks]
+    if graph:
+        for sr, st in zip(ranks, streams):
+            sr.capture(st)
+    for _ in range(steps):
+        for sr, st in zip(ranks, streams):
+            sr.step(stream=st)
+    torch.cuda.synchronize()
+    plan = ranks[0].plan
+    bad = []
+    for nm in sorted({n for w in ws for n in w.write_arrays}):
+        got = np.concatenate([to_host(sr.owned_slice(nm)) for sr in ranks], axis=0)
+        if not np.array_equal(got.view(np.uint64), g[nm][plan.glo:plan.ghi].view(np.uint64)):
+            bad.append(nm)
+    assert not bad, f"{nest} x{nranks}: {bad} differ from the single domain"
+
+
+@pytest.mark.parametrize("nest,size,nranks", [("swim", (24, 70), 2), ("swim", (27, 37), 3), ("clover", (22, 70), 3)])
+def test_sharded_pipeline_message_passing(nest, size, nranks):
+    """The NCCL path of a multi-kernel step (each kernel's written rows
+    exchanged before the next kernel), with the in-process thread shim."""
+    import threading
+    torch = _torch()
+    steps = 3
+    g, ws = single_pipeline(nest, size, steps)
+    ids = shard.PIPELINES[nest]
+    shim = _ThreadP2P(nranks)
+    ranks = [shard.SlabRank(ids, size, nranks, r, schedule="tiled") for r in range(nranks)]
+    for r, sr in enumerate(ranks):
+        sr.connect_p2p(shim.bind(r))
+    torch.cuda.synchronize()
+    errs = []
+
+    def run(sr):
+        try:
+            st = torch.cuda.Stream()
+            for _ in range(steps):
+                sr.step(stream=st)
+            st.synchronize()
+        except Exception as e:   # surfaced below
+            errs.append(e)
+            shim.bar.abort()
+    th = [threading.Thread(target=run, args=(sr,)) for sr in ranks]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs, errs
+    torch.cuda.synchronize()
+    plan = ranks[0].plan
+    for nm in sorted({n for w in ws for n in w.write_arrays}):
+        got = np.concatenate([to_host(sr.owned_slice(nm)) for sr in ranks], axis=0)
+        assert np.array_equal(got.view(np.uint64), g[nm][plan.glo:plan.ghi].view(np.uint64)), nm

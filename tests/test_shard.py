@@ -134,3 +134,73 @@ def test_gloo_ranks_equal_single_domain(kid, size, steps, nranks):
     plan = shard.plan_for(w, nranks)
     want = g[final][plan.glo:plan.ghi]
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_exchange_rows_swim_pattern():
+    """swim calc1 writes cv/z at j+1: rank r sends row own_hi to the upper
+    neighbour and never row own_hi-1 (outside the upper's buffer)."""
+    w = nests.workload("swim.c:calc1:0", (12, 9))
+    plan = shard.plan_for(w, 3)             # owned [0,4) [4,8) [8,12), reach (0, 1)
+    ops = dict((p, (s, r)) for p, s, r in shard.exchange_rows(plan, 1, 1, 1))
+    assert ops[2] == ((8, 9), (9, 9))       # send row 8 up, nothing comes down for a j+1 store
+    assert ops[0] == ((5, 5), (4, 5))       # lower's row 4 arrives
+    ops0 = dict((p, (s, r)) for p, s, r in shard.exchange_rows(plan, 1, 0, 0))
+    assert ops0[0] == ((4, 5), (4, 4)) and ops0[2] == ((8, 8), (8, 9))
+
+
+def _pipeline_worker(rank, nranks, port, nest, size, steps, q):
+    """A multi-kernel step (swim calc1->calc2->calc3, CloverLeaf ideal_gas ->
+    PdV -> advec) on one rank's rows: every kernel through the CPU oracle on
+    the slab, then its written rows exchanged with shard.p2p_exchange over the
+    rows shard.exchange_rows names — the NCCL path of SlabRank.connect_p2p."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=nranks)
+    from paper_2306_13002_b200 import backend, pipeline_exec
+    ids = shard.PIPELINES[nest]
+    g, ws = nests.pipeline_inputs(ids, size)
+    plan = shard.plan_for(ws[0], nranks)
+    o, n = plan.origin(rank), plan.local_planes(rank)
+    loc = {k: np.ascontiguousarray(v[o:o + n]).copy() if v.ndim >= 2 else v.copy() for k, v in g.items()}
+    reach = [pipeline_exec.reaches(backend.Kernel.lookup(k)) for k in ids]
+    for _ in range(steps):
+        for ki, w in enumerate(ws):
+            lw = shard.local_workload(w, plan, rank)
+            oracle_cpu.run(w.spec, {p.name: loc[p.name] for p in w.spec.arrays}, lw.scalars, "accsat", fma=True)
+            for name in w.write_arrays:
+                r = reach[ki][name]
+                ops = [(peer, (a - o, b - o), (c - o, d - o))
+                       for peer, (a, b), (c, d) in shard.exchange_rows(plan, rank, r.st_lo, r.st_hi)]
+                shard.p2p_exchange(dist, torch.from_numpy(loc[name]), ops)
+    lo, hi = plan.owned(rank)
+    written = sorted({nm for w in ws for nm in w.write_arrays})
+    part = {nm: loc[nm][lo - o:hi - o] for nm in written}
+    parts = [None] * nranks
+    dist.all_gather_object(parts, part)
+    if rank == 0:
+        q.put({nm: np.concatenate([p[nm] for p in parts], axis=0) for nm in written})
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nest,size,steps,nranks", [("swim", (13, 17), 3, 2), ("swim", (14, 9), 2, 3),
+                                                    ("clover", (11, 13), 2, 2)])
+def test_gloo_pipeline_equals_single_domain(nest, size, steps, nranks):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipeline_worker, args=(r, nranks, port, nest, size, steps, q))
+             for r in range(nranks)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ids = shard.PIPELINES[nest]
+    g, ws = nests.pipeline_inputs(ids, size)
+    for _ in range(steps):
+        for w in ws:
+            oracle_cpu.run(w.spec, {p.name: g[p.name] for p in w.spec.arrays}, w.scalars, "accsat", fma=True)
+    plan = shard.plan_for(ws[0], nranks)
+    for nm, arr in got.items():
+        want = g[nm][plan.glo:plan.ghi]
+        assert np.array_equal(arr.view(np.uint64), want.view(np.uint64)), nm
