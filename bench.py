@@ -42,9 +42,12 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 METRIC = "per-kernel GB/s (% B200 HBM roofline), saturated vs original speedup, 1/2/4/8 GPU"
 
 WORKLOADS = {
-    # name: (kernel id, dtype, grid per --size default, scaling)
+    # name: (kernel id(s), dtype, grid per --size default, scaling)
     "wave4": ("wave4.c:wave4:0", "f32", 1024, "strong"),
     "d3q19": ("d3q19.c:stream_collide:0", "f64", 256, "weak"),
+    # multi-kernel time steps of the 2-D nests (BASELINE configs[2], configs[3])
+    "swim": (["swim.c:calc1:0", "swim.c:calc2:1", "swim.c:calc3:2"], "f64", 8192, "strong"),
+    "clover": (["clover.c:ideal_gas:0", "clover.c:pdv_predict:1", "clover.c:advec_cell_x:2"], "f64", 7680, "strong"),
 }
 
 # per-kernel table: (kernel id, BASELINE size, dtype, sweeps per step)
@@ -134,6 +137,14 @@ def workload_config(workload, size, ws, variant):
         name = ("seismic wave4 4th-order 3-D acoustic wave propagation fp32 (BASELINE configs[4]), "
                 "one time step per step, 3-level buffer rotation")
         bpp = 16
+    elif workload == "swim":
+        grid = [size] * 2
+        name = "swim shallow-water time step calc1 -> calc2 -> calc3 fp64 (BASELINE configs[2])"
+        bpp = 56 + 80 + 120
+    elif workload == "clover":
+        grid = [size] * 2
+        name = "CloverLeaf-style hydro step ideal_gas -> PdV -> advec_cell_x fp64 (BASELINE configs[3])"
+        bpp = 32 + 96 + 48
     else:
         grid = [size, size, size * ws]
         name = ("D3Q19 lattice-Boltzmann collide+stream (olbm-like) fp64 (BASELINE configs[1]), "
@@ -244,13 +255,17 @@ def main():
     rank, ws, local, dist = dist_setup(args)
     peak, peak_kind = load_peaks()
     kid, dtype, _, scaling = WORKLOADS[args.workload]
-    size = (args.size,) * 3 if args.workload == "wave4" else (args.size * ws, args.size, args.size)
+    size = {"wave4": (args.size,) * 3, "d3q19": (args.size * ws, args.size, args.size)}.get(
+        args.workload, (args.size, args.size))
     sr = shard.SlabRank(kid, size, ws, rank, dtype=dtype, variant=args.variant, schedule=args.schedule)
     stream = torch.cuda.current_stream()
     tuned = None
     if args.schedule == "default" and args.variant != "original":
-        tuned, tuned_ms = sr.k.tune(sr.buf, dict(sr.w.scalars), args.variant, reps=5)   # untimed autotune
-        sr.schedule = tuned
+        tuned = []
+        for k, lw in zip(sr.ks, sr.ws):                                  # untimed autotune, per kernel
+            names = [a.name for a in lw.spec.arrays]
+            tuned.append(k.tune({n: sr.buf[n] for n in names}, dict(lw.scalars), args.variant, reps=5)[0])
+        sr.schedule = tuned if sr.multi else tuned[0]
         sr.refill()
     torch.cuda.synchronize()
     exchange = "none"
@@ -264,19 +279,18 @@ def main():
         graph = True
     if dist:
         dist.barrier()
-    per_step = {"none": 1, "peer": 3, "p2p": None}[sr.mode]
-    if per_step is None:
-        per_step = 1 + (rank > 0) + (rank < ws - 1)       # interior + boundary slabs
+    per_step = sr.launches_per_step()
     for _ in range(args.warmup):
         sr.step(stream=stream)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ms = time_steps(lambda: sr.step(stream=stream), args.steps, 0, stream, dist)
-    local_bytes = sr.w.algorithmic_bytes
-    total_bytes = sr.gw.algorithmic_bytes
+    local_bytes = sr.algorithmic_bytes
+    total_bytes = sr.global_bytes
     value = total_bytes / (ms * 1e-3) / 1e9
-    slot = sr.schedule if isinstance(sr.schedule, int) else None
-    sched_name = sr.k.info["schedules"][1 if dtype == "f32" else 0][slot] if slot is not None else str(sr.schedule)
+    scheds = sr.schedule if isinstance(sr.schedule, list) else [sr.schedule]
+    sched_name = "; ".join(k.info["schedules"][1 if dtype == "f32" else 0][sc] if isinstance(sc, int) else str(sc)
+                           for k, sc in zip(sr.ks, scheds))
     out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": scaling,
            "vs_baseline": None, "dtype": dtype,
@@ -294,16 +308,17 @@ def main():
                          "layout": "row-major, 16-element padded pitch, sector-aligned rows"
                                    if args.workload == "wave4" else "q-major SoA"}}
     achieved = local_bytes / (ms * 1e-3) / 1e9
-    kname = "wave4_f32" if args.workload == "wave4" else "stream_collide"
+    kname = {"wave4": "wave4_f32", "d3q19": "stream_collide", "swim": "calc1+calc2+calc3",
+             "clover": "ideal_gas+pdv_predict+advec_cell_x"}[args.workload]
     out["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                        "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
                        "traffic": load_traffic(kname),
                        "kernel": f"{kname} {args.variant}: {sched_name}",
-                       "per_unit": f"{sr.w.bytes_per_point} B/point x {sr.w.points} points per launch "
-                                   "(rank 0's slab), over the step's CUDA-event time"}
+                       "per_unit": f"{sum(lw.bytes_per_point for lw in sr.ws)} B/point x {sr.w.points} points "
+                                   "per step (rank 0's slab), over the step's CUDA-event time"}
     out["clocks"] = clk.summary()
     if not args.no_e2e:
-        if ws == 1:
+        if ws == 1 and not sr.multi:
             sr.close()
             del sr.buf
             torch.cuda.empty_cache()
@@ -367,18 +382,24 @@ def e2e_sharded(args, sr, dist, ws):
     stream = torch.cuda.current_stream()
     names = sr.names
     lo, hi = sr.plan.local_range(sr.rank)
-    ins = [n for n in names if n in sr.w.read_arrays and len(sr.w.dims[n]) >= 2]
+    produced = {n for lw in sr.ws for n in lw.write_arrays}
+    ins = [n for n in names if any(n in lw.read_arrays for lw in sr.ws) and len(sr.buf[n].shape) >= 2]
     host = {n: torch.empty(tuple(sr.buf[n].shape), dtype=sr.buf[n].dtype, pin_memory=True) for n in names}
     rm = {n: torch.empty(tuple(sr.buf[n].shape), dtype=sr.buf[n].dtype, device="cuda") for n in names}
     for n in names:
         backend.copy(rm[n], sr.buf[n])
         host[n].copy_(rm[n])
     torch.cuda.synchronize()
-    out_name = sr.w.write_arrays[0]      # the produced array: D3Q19 dst, wave4 un
+    # the step's results: single-kernel nests their produced array (D3Q19 dst,
+    # wave4 un); multi-kernel steps every array a kernel writes
+    outs = sorted(produced) if sr.multi else [sr.w.write_arrays[0]]
     sr.graphs = None                     # eager: the uploads go between wait and launch
 
+    def roles_at(s):
+        return {n: n for n in names} if sr.multi else nests.role_buffers(sr.nest, names, s)
+
     def upload(s, h):
-        roles = nests.role_buffers(sr.nest, names, s)
+        roles = roles_at(s)
         for p in ins:
             rm[p][lo:hi].copy_(host[p][lo:hi], non_blocking=True)
             backend.copy(sr.buf[roles[p]][lo:hi], rm[p][lo:hi], stream)
@@ -386,15 +407,16 @@ def e2e_sharded(args, sr, dist, ws):
     def step():
         s = sr.step_no
         sr.step(stream=stream, before_launch=upload)
-        roles = nests.role_buffers(sr.nest, names, s)
-        backend.copy(rm[out_name][lo:hi], sr.buf[roles[out_name]][lo:hi], stream)
-        host[out_name][lo:hi].copy_(rm[out_name][lo:hi], non_blocking=True)
+        roles = roles_at(s)
+        for o in outs:
+            backend.copy(rm[o][lo:hi], sr.buf[roles[o]][lo:hi], stream)
+            host[o][lo:hi].copy_(rm[o][lo:hi], non_blocking=True)
 
     steps = max(3, min(args.steps, 10))
     ms = time_steps(step, steps, 2, stream, dist)
     h2d = sum(host[n][lo:hi].numel() * host[n].element_size() for n in ins)
-    d2h = host[out_name][lo:hi].numel() * host[out_name].element_size()
-    total = sr.gw.algorithmic_bytes
+    d2h = sum(host[o][lo:hi].numel() * host[o].element_size() for o in outs)
+    total = sr.global_bytes
     return {"value": round(total / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3), "steps": steps,
             "path": "per rank: owned planes of the inputs, pinned host (reference layout) -> H2D -> remap -> "
@@ -577,51 +599,71 @@ def mem_available():
 
 
 def cpu_workload(args):
-    """The workload the CPU runs: the full configured grid when the host has
-    the memory for it (wave4 1024^3 fp32: 17.4 GB), else a 512^3 sample."""
+    """The workloads (one per kernel of the step) the CPU runs: the full
+    configured grid when the host has the memory for it (wave4 1024^3 fp32:
+    17.4 GB), else a 512^3 (2-D: 4096^2) sample."""
     from paper_2306_13002_b200 import nests
     kid, dtype, _, _ = WORKLOADS[args.workload]
+    ids = [kid] if isinstance(kid, str) else kid
     n = args.size
-    w = nests.workload(kid, n, dtype=dtype)
-    need = sum(int(np.prod(d)) for d in w.dims.values()) * (4 if dtype == "f32" else 8)
+    ws = [nests.workload(k, n, dtype=dtype) for k in ids]
+    dims = {}
+    for w in ws:
+        dims.update(w.dims)
+    need = sum(int(np.prod(d)) for d in dims.values()) * (4 if dtype == "f32" else 8)
     if mem_available() < 2 * need + (8 << 30):
-        n = min(args.size, 512)
-        w = nests.workload(kid, n, dtype=dtype)
-    return w, n
+        n = min(args.size, 512 if len(ws[0].spec.loop_vars) == 3 else 4096)
+        ws = [nests.workload(k, n, dtype=dtype) for k in ids]
+    return ws, n
 
 
-def run_cpu_steps(w, variant, steps, threads, arrays):
-    """Timed steps of the reference's CPU path, buffers rotating like the GPU
-    steps (D3Q19 src <-> dst, wave4 up <- u <- un)."""
+def cpu_inputs(ws, threads):
+    """Host inputs of the step (union of its kernels' arrays, first kernel
+    that declares an array fills it), generated by oracle/fill.c."""
+    import cpu as oracle_cpu
+    out = {}
+    for w in ws:
+        for n, a in oracle_cpu.host_inputs(w, threads).items():
+            out.setdefault(n, a)
+    return out
+
+
+def run_cpu_steps(ws, variant, steps, threads, arrays):
+    """Timed steps of the reference's CPU path: every kernel of the step in
+    order, buffers rotating like the GPU steps (D3Q19 src <-> dst, wave4
+    up <- u <- un)."""
     import cpu as oracle_cpu
     from paper_2306_13002_b200 import nests
     names = list(arrays)
     ts = []
     for s in range(steps):
-        roles = nests.role_buffers(w.spec.nest, names, s)
-        a = {p: arrays[roles[p]] for p in names}
+        roles = nests.role_buffers(ws[0].spec.nest, names, s) if len(ws) == 1 else {n: n for n in names}
         t0 = time.perf_counter()
-        oracle_cpu.run(w.spec, a, w.scalars, variant, threads=threads, f32=w.dtype == "f32", ref=True)
+        for w in ws:
+            a = {p.name: arrays[roles[p.name]] for p in w.spec.arrays}
+            oracle_cpu.run(w.spec, a, w.scalars, variant, threads=threads, f32=w.dtype == "f32", ref=True)
         ts.append(time.perf_counter() - t0)
     return ts
 
 
-def cpu_sample_desc(n, steps):
-    return f"{steps} steps of the {n}^3 grid"
+def cpu_sample_desc(n, steps, ws):
+    return f"{steps} steps of the {n}^{len(ws[0].spec.loop_vars)} grid" + (
+        f" ({' -> '.join(w.spec.function for w in ws)} per step)" if len(ws) > 1 else "")
 
 
 def cpu_baseline(args):
     import cpu as oracle_cpu
-    w, n = cpu_workload(args)
+    ws, n = cpu_workload(args)
     threads = cpu_threads(args)
-    arrays = oracle_cpu.host_inputs(w, threads)
-    run_cpu_steps(w, args.variant, 1, threads, arrays)            # first touch
-    ts = run_cpu_steps(w, args.variant, 3, threads, arrays)
+    arrays = cpu_inputs(ws, threads)
+    nbytes = sum(w.algorithmic_bytes for w in ws)
+    run_cpu_steps(ws, args.variant, 1, threads, arrays)            # first touch
+    ts = run_cpu_steps(ws, args.variant, 3, threads, arrays)
     t = float(np.median(ts))
-    t1 = run_cpu_steps(w, args.variant, 1, 1, arrays)            # one core, one step (SURVEY §8d)
-    return {"value": round(w.algorithmic_bytes / t / 1e9, 3), "unit": "GB/s", "cores": threads,
-            "value_1core": round(w.algorithmic_bytes / t1[0] / 1e9, 3), "kind": "reference",
-            "sample": f"{cpu_sample_desc(n, 3)} (median) of the reference-emitted {args.variant} C "
+    t1 = run_cpu_steps(ws, args.variant, 1, 1, arrays)            # one core, one step (SURVEY §8d)
+    return {"value": round(nbytes / t / 1e9, 3), "unit": "GB/s", "cores": threads,
+            "value_1core": round(nbytes / t1[0] / 1e9, 3), "kind": "reference",
+            "sample": f"{cpu_sample_desc(n, 3, ws)} (median) of the reference-emitted {args.variant} C "
                       "(gcc -O3 -ffp-contract=off, OpenMP over the outermost loop); value_1core: one step, one thread",
             "cpu": cpu_model()}
 
@@ -644,24 +686,24 @@ def reference_arm(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    import cpu as oracle_cpu
-    w, n = cpu_workload(args)
+    wl, n = cpu_workload(args)
     threads = cpu_threads(args)
-    arrays = oracle_cpu.host_inputs(w, threads)                  # host generator: no GPU library
-    run_cpu_steps(w, args.variant, args.warmup, threads, arrays)
-    ts = run_cpu_steps(w, args.variant, args.steps, threads, arrays)
+    arrays = cpu_inputs(wl, threads)                             # host generator: no GPU library
+    run_cpu_steps(wl, args.variant, args.warmup, threads, arrays)
+    ts = run_cpu_steps(wl, args.variant, args.steps, threads, arrays)
     t = sum(ts) / len(ts)
     cfg = workload_config(args.workload, args.size, ws, args.variant)
     total = cfg["points"] * cfg["bytes_per_point"]
     # GB/s of the steps the CPU ran (a sample when the full grid does not fit)
-    v = w.algorithmic_bytes / t / 1e9
+    nbytes = sum(w.algorithmic_bytes for w in wl)
+    v = nbytes / t / 1e9
     out = {"metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(t * 1e3 * total / w.algorithmic_bytes, 2),
+           "warmup": args.warmup, "ms_per_step": round(t * 1e3 * total / nbytes, 2),
            "higher_is_better": True, "scaling": cfg["scaling"], "vs_baseline": None, "dtype": cfg["dtype"],
            "data": "synthetic (seeded SplitMix64, SURVEY.md §8d distributions; identical values to our arm)",
            "impl": "reference", "config": cfg,
            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-                            "sample": f"{cpu_sample_desc(n, args.steps)} (after {args.warmup} warm-up steps); "
+                            "sample": f"{cpu_sample_desc(n, args.steps, wl)} (after {args.warmup} warm-up steps); "
                                       f"reference-emitted {args.variant} C compiled by gcc -O3 -ffp-contract=off "
                                       "(satcc wrapper mode), OpenMP over the outermost loop",
                             "cpu": cpu_model()},
