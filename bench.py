@@ -264,7 +264,7 @@ def main():
         tuned = []
         for k, lw in zip(sr.ks, sr.ws):                                  # untimed autotune, per kernel
             names = [a.name for a in lw.spec.arrays]
-            tuned.append(k.tune({n: sr.buf[n] for n in names}, dict(lw.scalars), args.variant, reps=5)[0])
+            tuned.append(k.tune({n: sr.buf[n] for n in names}, dict(lw.scalars), args.variant, reps=15)[0])
         sr.schedule = tuned if sr.multi else tuned[0]
         sr.refill()
     torch.cuda.synchronize()
@@ -482,7 +482,7 @@ def tune_kernel(kid, size, dtype, variant):
     w = nests.workload(kid, size, dtype=dtype)
     k = backend.Kernel.lookup(kid)
     arrs = nests.device_inputs(w, native=True, kernel=k)
-    best, ms = k.tune(arrs, dict(w.scalars), variant, reps=5)
+    best, ms = k.tune(arrs, dict(w.scalars), variant, reps=15)
     name = k.info["schedules"][1 if dtype == "f32" else 0][best]
     del arrs
     torch.cuda.empty_cache()

@@ -10,6 +10,7 @@
 #include "registry.hpp"
 #include "tma.cuh"
 
+#include <algorithm>
 #include <cstring>
 
 namespace acs {
@@ -618,17 +619,26 @@ acs_status acs_tune(const acs_kernel* k, acs_variant variant, const acs_array* a
             cudaEventDestroy(e1);
             return st;
         }
-        cudaEventRecord(e0, s);
-        for (int i = 0; i < reps; ++i) fn(r);
-        cudaEventRecord(e1, s);
-        if (cudaEventSynchronize(e1) != cudaSuccess) {
+        // per-launch events, median: one slow launch (clock or power-cap
+        // transient) must not decide the slot
+        std::vector<cudaEvent_t> ev((size_t)reps + 1);
+        for (auto& x : ev) cudaEventCreate(&x);
+        cudaEventRecord(ev[0], s);
+        for (int i = 0; i < reps; ++i) {
+            fn(r);
+            cudaEventRecord(ev[i + 1], s);
+        }
+        if (cudaEventSynchronize(ev[reps]) != cudaSuccess) {
+            for (auto& x : ev) cudaEventDestroy(x);
             cudaEventDestroy(e0);
             cudaEventDestroy(e1);
             return check_launch("acs_tune");
         }
-        float ms = 0;
-        cudaEventElapsedTime(&ms, e0, e1);
-        ms /= reps;
+        std::vector<float> t((size_t)reps);
+        for (int i = 0; i < reps; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+        for (auto& x : ev) cudaEventDestroy(x);
+        std::sort(t.begin(), t.end());
+        const float ms = reps % 2 ? t[reps / 2] : 0.5f * (t[reps / 2 - 1] + t[reps / 2]);
         if (ms_per_launch) ms_per_launch[slot] = ms;
         if (ms < best) {
             best = ms;
