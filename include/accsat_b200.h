@@ -176,7 +176,7 @@ const char* acs_kernel_schedule_name(const acs_kernel* k, int precision, int slo
  * repeated launches), records the fastest as what ACS_SCHED_DEFAULT /
  * ACS_SCHED_TILED use for this (kernel, precision, variant) from now on, and
  * returns it.  ms_per_launch[slot] (optional, kMaxSched=8 entries) receives
-XX
+ * the timings (negative = slot absent).  Synchronous. */
 acs_status acs_tune(const acs_kernel* k, acs_variant variant, const acs_array* arrays, int n_arrays,
                     const acs_scalar* scalars, int n_scalars, void* cuda_stream, int reps, int* best_slot,
                     float* ms_per_launch);
