@@ -267,19 +267,28 @@ def copy(dst, src, stream=None) -> None:
     _check(lib().acs_copy(ctypes.byref(a), ctypes.byref(b), _stream_handle(stream)), "acs_copy")
 
 
-def empty_native(kernel: Kernel, name: str, dims, dtype, device="cuda"):
+def native_offset(kernel: Kernel, name: str, esize: int) -> int:
+    off = ctypes.c_int64()
+    f = lib().acs_native_offset
+    f.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_void_p]
+    _check(f(kernel.handle, name.encode(), esize, ctypes.byref(off)), "acs_native_offset")
+    return off.value
+
+
+def empty_native(kernel: Kernel, name: str, dims, dtype, device="cuda", shared_with=()):
     """Device tensor with the backend's preferred strides and start offset for
-    `name` (acs_native_strides / acs_native_offset)."""
+    `name` (acs_native_strides / acs_native_offset).  `shared_with`: other
+    kernels that read the same array; when their preferred start offsets
+    differ the array starts 16-byte aligned (every skeleton takes that)."""
     torch = _torch()
     st = kernel.native_strides(name, tuple(dims))
     n = int(np.prod(dims))
     if not n:
         return torch.empty(tuple(dims), dtype=dtype, device=device)
     esize = torch.empty((), dtype=dtype).element_size()
-    off = ctypes.c_int64()
-    f = lib().acs_native_offset
-    f.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_void_p]
-    _check(f(kernel.handle, name.encode(), esize, ctypes.byref(off)), "acs_native_offset")
+    off = ctypes.c_int64(native_offset(kernel, name, esize))
+    if any(native_offset(k, name, esize) != off.value for k in shared_with):
+        off = ctypes.c_int64(0)
     if off.value == 0:
         return torch.empty_strided(tuple(dims), st, dtype=dtype, device=device)
     span = 1 + sum((d - 1) * s for d, s in zip(dims, st))

@@ -450,7 +450,7 @@ static acs_status launch_impl(const acs_kernel* k, acs_variant variant, acs_sche
         return ACS_E_NO_KERNEL;
     }
     LaunchReq r{arrays, n_arrays, scalars, n_scalars, static_cast<cudaStream_t>(cuda_stream), shard,
-                schedule != ACS_SCHED_DEFAULT && schedule != ACS_SCHED_NAIVE};
+                (int)schedule >= 16};   // an explicit slot fails loudly on a layout it cannot take
     return fn(r);
 }
 

@@ -351,12 +351,13 @@ class SlabRank:
         for name, (p, lw) in self.arrays.items():
             dims = lw.dims[name]
             dt = torch.int32 if p.ctype == "int" else tdt
-            k = next(kk for kk, w in zip(self.ks, self.ws) if name in [a.name for a in w.spec.arrays])
+            users = [kk for kk, w in zip(self.ks, self.ws) if name in [a.name for a in w.spec.arrays]]
+            k, others = users[0], users[1:]
             if len(dims) >= 2:
-                full = backend.empty_native(k, name, (maxp,) + tuple(dims[1:]), dt)
+                full = backend.empty_native(k, name, (maxp,) + tuple(dims[1:]), dt, shared_with=others)
                 t = full[:dims[0]]
             else:
-                t = backend.empty_native(k, name, dims, dt)
+                t = backend.empty_native(k, name, dims, dt, shared_with=others)
             out[name] = t
         self.refill(out)
         return out
