@@ -228,6 +228,13 @@ acs_status acs_wait(const uint64_t* flag_a, const uint64_t* flag_b, uint64_t val
 acs_status acs_signal_ctr(uint64_t* flag_a, uint64_t* flag_b, uint64_t* counter, void* cuda_stream);
 acs_status acs_wait_ctr(const uint64_t* flag_a, const uint64_t* flag_b, const uint64_t* counter, int timeout_ms,
                         void* cuda_stream);
+/* eval_region for HOST arrays (row-major, the reference layout; `data` =
+ * host pointers): uploads every array, runs the whole nest with the DEFAULT
+ * schedule, downloads every array the nest stores, synchronously.  The call a
+ * program compiled through the B200 wrapper hand-off makes in place of the
+ * nest's loops (paper_2306_13002_b200/jit.py). */
+acs_status acs_eval_host(const acs_kernel* k, acs_variant variant, const acs_array* host_arrays, int n_arrays,
+                         const acs_scalar* scalars, int n_scalars);
 /* Loads the code of every schedule slot of (kernel, variant) for these arrays
  * without launching anything.  CUDA lazy loading loads a kernel at its first
  * launch and may wait for the device to drain: call this before a sharded

@@ -15,12 +15,18 @@
 
 namespace acs {
 
+#ifdef ACS_JIT_REGISTRY
+// a library built by paper_2306_13002_b200/jit.py for one user nest file:
+// its generated registration unit defines register_jit()
+void register_jit();
+#else
 void register_jacobi7();
 void register_swim();
 void register_clover();
 void register_wave4();
 void register_d3q19();
 void register_zsolve();
+#endif
 
 namespace {
 thread_local std::string g_err;
@@ -31,12 +37,16 @@ std::vector<Entry*>& registry() {
 std::once_flag g_once;
 void init_registry() {
     std::call_once(g_once, [] {
+#ifdef ACS_JIT_REGISTRY
+        register_jit();
+#else
         register_jacobi7();
         register_swim();
         register_clover();
         register_wave4();
         register_d3q19();
         register_zsolve();
+#endif
     });
 }
 }  // namespace
@@ -478,6 +488,61 @@ acs_status acs_wait(const uint64_t* flag_a, const uint64_t* flag_b, uint64_t val
                                                                     (const unsigned long long*)flag_b, value,
                                                                     (unsigned long long)timeout_ms * 1000000ULL);
     return check_launch("acs_wait");
+}
+
+acs_status acs_eval_host(const acs_kernel* k, acs_variant variant, const acs_array* host, int n_arrays,
+                         const acs_scalar* scalars, int n_scalars) {
+    if (!k || (n_arrays > 0 && !host) || (n_scalars > 0 && !scalars)) {
+        set_error("acs_eval_host: null argument");
+        return ACS_E_ARG;
+    }
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    static const int esize[5] = {8, 4, 4, 8, 1};
+    std::vector<acs_array> dev(host, host + n_arrays);
+    std::vector<void*> bufs((size_t)n_arrays, nullptr);
+    std::vector<size_t> bytes((size_t)n_arrays, 0);
+    auto fail = [&](const std::string& what, cudaError_t err) {
+        for (void* b : bufs)
+            if (b) cudaFree(b);
+        set_error("acs_eval_host: " + what + ": " + cudaGetErrorString(err));
+        return ACS_E_CUDA;
+    };
+    for (int i = 0; i < n_arrays; ++i) {
+        const acs_array& a = host[i];
+        if ((int)a.dtype < 0 || (int)a.dtype > 4 || a.ndim < 1 || a.ndim > ACS_MAX_DIMS || !a.data) {
+            set_error(std::string("acs_eval_host: bad array '") + (a.name ? a.name : "") + "'");
+            return ACS_E_ARG;
+        }
+        size_t n = 1;
+        for (int p = 0; p < a.ndim; ++p) {
+            if (a.strides[p] != 0) {
+                set_error("acs_eval_host: host arrays are row-major (strides 0)");
+                return ACS_E_ARG;
+            }
+            n *= (size_t)a.dims[p];
+        }
+        bytes[i] = n * (size_t)esize[a.dtype];
+        cudaError_t err = cudaMalloc(&bufs[i], bytes[i] ? bytes[i] : 1);
+        if (err != cudaSuccess) return fail("cudaMalloc", err);
+        err = cudaMemcpy(bufs[i], a.data, bytes[i], cudaMemcpyHostToDevice);
+        if (err != cudaSuccess) return fail("upload", err);
+        dev[i].data = bufs[i];
+    }
+    acs_status st = launch_impl(k, variant, ACS_SCHED_DEFAULT, dev.data(), n_arrays, scalars, n_scalars, nullptr,
+                                nullptr);
+    cudaError_t err = cudaDeviceSynchronize();
+    if (st == ACS_OK && err != cudaSuccess) return fail("launch", err);
+    for (int i = 0; i < n_arrays && st == ACS_OK; ++i) {
+        bool stored = true;   // unknown names: copy back (the post-state keeps every array)
+        for (size_t a = 0; a < e->arrays.size(); ++a)
+            if (host[i].name && e->arrays[a] == host[i].name) stored = e->reach[a].stored;
+        if (!stored) continue;
+        err = cudaMemcpy(host[i].data, bufs[i], bytes[i], cudaMemcpyDeviceToHost);
+        if (err != cudaSuccess) return fail("download", err);
+    }
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    return st;
 }
 
 acs_status acs_preload(const acs_kernel* k, acs_variant variant, const acs_array* arrays, int n_arrays,

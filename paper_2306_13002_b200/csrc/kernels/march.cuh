@@ -1269,4 +1269,17 @@ void fill_march(Entry& e, int prec) {
         if (e.best[prec][v] == 0 && v != ACS_ORIGINAL) e.best[prec][v] = slot;
 }
 
+// Default skeleton set of a nest registered at run time (paper_2306_13002_b200/
+// jit.py): naive, and the TMA march skeleton when the nest's loads are stageable.
+template <class NS, class T>
+void fill_default(Entry& e) {
+    fill_naive<NS, T>(e, 0);
+    if constexpr (NS::NLOOP == 3) {
+        if constexpr (MarchPlan<NS, T, 0, 128, 4, 1>::usable()) fill_march<NS, T, 0, 128, 4, 128, 2, 3>(e, 0);
+    } else if constexpr (NS::NLOOP == 2) {
+        fill_naive_multi<NS, T, 2>(e, 0);
+        if constexpr (MarchPlan<NS, T, 0, 128, 1, 1>::usable()) fill_march<NS, T, 0, 128, 1, 128, 1, 3>(e, 0);
+    }
+}
+
 }  // namespace acs

@@ -7,11 +7,13 @@
 //                                                       satcc-verify-v1 JSON: differential
 //        run of original vs optimized region bodies under the reference's
 //        interpreter semantics (diff_test, proj/src/oracle.cpp:12-81)
-//   acs-satcc [--variant V] [--keep] -- cmd args...     wrapper mode: every
+//   acs-satcc [--variant V] [--keep] [--backend cc|b200] -- cmd args...
+//                                                       wrapper mode: every
 //        existing *.c argument is optimized into <tmp>/<argidx>/<basename> and
 //        cmd runs on the substituted paths; exit code propagated (128+signal,
 //        127 if exec fails); an unparseable file passes through unchanged
-//        (satcc_main.cpp:285-360).
+//        (satcc_main.cpp:285-360).  --backend b200: the nest functions of
+//        every file run on the B200 instead (paper_2306_13002_b200/jit.py).
 //
 // Flags: --variant (cse | cse+sat | cse+bulk | accsat, default accsat),
 // --max-nodes, --sat-time, --iters, --extract greedy|dag, --no-sat, --no-bulk.
@@ -43,6 +45,7 @@ int main(int argc, char** argv) {
     std::string cmd = "opt", variant = "accsat", output;
     acs_opt_limits lim{10000, 10.0, 10, 1};
     bool no_sat = false, no_bulk = false, keep = false;
+    std::string backend = "cc";   // cc: hand the optimized C to the wrapped compiler; b200: to this backend
     std::vector<std::string> files, child;
     size_t i = 0;
     if (!args.empty() && (args[0] == "opt" || args[0] == "report" || args[0] == "verify")) cmd = args[i++];
@@ -70,6 +73,7 @@ int main(int argc, char** argv) {
         else if (a == "--no-sat") no_sat = true;
         else if (a == "--no-bulk") no_bulk = true;
         else if (a == "--keep") keep = true;
+        else if (a == "--backend") backend = next();
         else if (a == "--trials") trials = std::stoi(next());
         else if (a == "--tol") tol_rel = std::stod(next());
         else files.push_back(a);
@@ -90,6 +94,26 @@ int main(int argc, char** argv) {
         return rc;
     };
 
+    if (cmd == "wrap" && backend == "b200") {
+        // the B200 as the downstream: paper_2306_13002_b200/jit.py builds the
+        // file's kernels and stubs the nest functions into acs_eval_host calls
+        std::string exe = argv[0];
+        std::string dir = exe.find_last_of('/') == std::string::npos ? "." : exe.substr(0, exe.find_last_of('/'));
+        std::string root = dir + "/..";
+        std::vector<std::string> py = {"python3", "-m", "paper_2306_13002_b200.jit", "wrap", "--variant", variant};
+        if (keep) py.push_back("--keep");
+        py.push_back("--");
+        py.insert(py.end(), child.begin(), child.end());
+        const char* pp = std::getenv("PYTHONPATH");
+        std::string path = root + (pp ? std::string(":") + pp : "");
+        setenv("PYTHONPATH", path.c_str(), 1);
+        std::vector<char*> av;
+        for (auto& x : py) av.push_back(const_cast<char*>(x.c_str()));
+        av.push_back(nullptr);
+        execvp(av[0], av.data());
+        std::cerr << "acs-satcc: cannot exec python3 for --backend b200\n";
+        return 127;
+    }
     if (cmd == "wrap") {
         if (child.empty()) {
             std::cerr << "acs-satcc: nothing to run after --\n";

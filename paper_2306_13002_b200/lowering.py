@@ -939,10 +939,17 @@ def _scalar_struct(params, f32):
     return lines
 
 
-def gen_function(nest: str, function: str, f32: bool = False) -> Tuple[str, dict]:
+def gen_function(nest: str, function: str, f32: bool = False, sources: Optional[Dict[str, str]] = None
+                 ) -> Tuple[str, dict]:
+    """Device bodies of every form of one nest function.  `sources` maps each
+    form's variant (None = the original) to its module text; default: the
+    benchmark nest's text and host stage (a)'s emitted files."""
     ns = function + ("_f32" if f32 else "")
     texts = {}
     for form, variant, fma in FORMS:
+        if sources is not None:
+            texts[form] = (sources[variant], fma)
+            continue
         path = os.path.join(ROOT, "nests", f"{nest}.c") if variant is None else stage_a.ensure(nest, variant)
         texts[form] = (open(path).read(), fma)
     lows = {form: lower_text(t, function, fma, f32) for form, (t, fma) in texts.items()}
