@@ -2,7 +2,10 @@
 // option-compatible with the reference CLI's core (proj/tools/satcc_main.cpp):
 //
 //   acs-satcc [opt] [--variant V] [-o FILE] file        optimized source
-//   acs-satcc report [--variant V] file...              satcc-metrics-v1 JSON
+//   acs-satcc report [--variant V] [--gpu [--size N]] file...
+//                                                       satcc-metrics-v1 JSON (--gpu: plus the
+//        B200 execution of every region: GB/s, roofline fraction, skeleton,
+//        saturated-vs-original difference; paper_2306_13002_b200/report.py)
 //   acs-satcc verify [--variant V] [--trials N] [--tol T] file...
 //                                                       satcc-verify-v1 JSON: differential
 //        run of original vs optimized region bodies under the reference's
@@ -46,6 +49,8 @@ int main(int argc, char** argv) {
     acs_opt_limits lim{10000, 10.0, 10, 1};
     bool no_sat = false, no_bulk = false, keep = false;
     std::string backend = "cc";   // cc: hand the optimized C to the wrapped compiler; b200: to this backend
+    bool gpu = false;             // report --gpu: satcc-metrics-v1 plus the B200 execution of every region
+    std::string size;
     std::vector<std::string> files, child;
     size_t i = 0;
     if (!args.empty() && (args[0] == "opt" || args[0] == "report" || args[0] == "verify")) cmd = args[i++];
@@ -74,6 +79,8 @@ int main(int argc, char** argv) {
         else if (a == "--no-bulk") no_bulk = true;
         else if (a == "--keep") keep = true;
         else if (a == "--backend") backend = next();
+        else if (a == "--gpu") gpu = true;
+        else if (a == "--size") size = next();
         else if (a == "--trials") trials = std::stoi(next());
         else if (a == "--tol") tol_rel = std::stod(next());
         else files.push_back(a);
@@ -94,25 +101,36 @@ int main(int argc, char** argv) {
         return rc;
     };
 
-    if (cmd == "wrap" && backend == "b200") {
-        // the B200 as the downstream: paper_2306_13002_b200/jit.py builds the
-        // file's kernels and stubs the nest functions into acs_eval_host calls
+    auto exec_python = [&](std::vector<std::string> py) -> int {
         std::string exe = argv[0];
         std::string dir = exe.find_last_of('/') == std::string::npos ? "." : exe.substr(0, exe.find_last_of('/'));
-        std::string root = dir + "/..";
-        std::vector<std::string> py = {"python3", "-m", "paper_2306_13002_b200.jit", "wrap", "--variant", variant};
-        if (keep) py.push_back("--keep");
-        py.push_back("--");
-        py.insert(py.end(), child.begin(), child.end());
         const char* pp = std::getenv("PYTHONPATH");
-        std::string path = root + (pp ? std::string(":") + pp : "");
+        std::string path = dir + "/.." + (pp ? std::string(":") + pp : "");
         setenv("PYTHONPATH", path.c_str(), 1);
         std::vector<char*> av;
         for (auto& x : py) av.push_back(const_cast<char*>(x.c_str()));
         av.push_back(nullptr);
         execvp(av[0], av.data());
-        std::cerr << "acs-satcc: cannot exec python3 for --backend b200\n";
+        std::cerr << "acs-satcc: cannot exec python3\n";
         return 127;
+    };
+    if (cmd == "report" && gpu) {
+        std::vector<std::string> py = {"python3", "-m", "paper_2306_13002_b200.report", "--gpu", "--variant", variant};
+        if (!size.empty()) {
+            py.push_back("--size");
+            py.push_back(size);
+        }
+        py.insert(py.end(), files.begin(), files.end());
+        return exec_python(py);
+    }
+    if (cmd == "wrap" && backend == "b200") {
+        // the B200 as the downstream: paper_2306_13002_b200/jit.py builds the
+        // file's kernels and stubs the nest functions into acs_eval_host calls
+        std::vector<std::string> py = {"python3", "-m", "paper_2306_13002_b200.jit", "wrap", "--variant", variant};
+        if (keep) py.push_back("--keep");
+        py.push_back("--");
+        py.insert(py.end(), child.begin(), child.end());
+        return exec_python(py);
     }
     if (cmd == "wrap") {
         if (child.empty()) {

@@ -40,3 +40,21 @@ def test_wrapped_program_runs_on_the_b200(variant):
         assert got == want
     else:
         assert abs(got[1] - want[1]) <= 1e-12 * abs(want[1])
+
+
+def test_report_gpu_fields():
+    """acs-satcc report --gpu: satcc-metrics-v1 plus each region's B200 run."""
+    import json
+    r = subprocess.run([SATCC, "report", "--gpu", "--size", "64", os.path.join(ROOT, "nests", "wave4.c"),
+                        os.path.join(ROOT, "nests", "swim.c")], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr
+    reps = json.loads(r.stdout)
+    regions = [g for rep in reps for g in rep["regions"]]
+    assert len(regions) == 4 and all(rep["schema"] == "satcc-metrics-v1" for rep in reps)
+    for g in regions:
+        gpu = g["gpu"]
+        assert "error" not in gpu, gpu
+        assert gpu["gbs"] > 0 and 0 < gpu["roofline_frac"] < 2 and gpu["schedule"]
+        assert gpu["static_loads"] == g["static_loads_after"] and gpu["fma_count"] == g["fma_count"]
+        # the saturated form's single-rounding FMAs vs the original's two roundings
+        assert gpu["vs_original"]["max_abs"] <= (1e-7 if gpu["dtype"] == "f32" else 1e-8), gpu
