@@ -139,6 +139,7 @@ class _Lowerer:
         self.capture: Optional[Dict[tuple, str]] = None   # if-conversion: store target -> value var
         self.capture_pair: Optional[Dict[tuple, str]] = None   # first arm's values (second arm stores)
         self.n_ifc = 0
+        self.seq_vars: set = set()      # scalars assigned inside sequential inner loops
         self.ifconv = ifconv
         self.plain = plain      # nvcc-default arithmetic: C operators, contraction left to the compiler
         self.body_stmt: Optional[ks.Stmt] = None
@@ -173,13 +174,26 @@ class _Lowerer:
         return "int" if a == b == "int" else "double"
 
     # -- affine resolution of subscripts
-    def count_assigns(self, s: ks.Stmt):
+    def count_assigns(self, s: ks.Stmt, in_loop: bool = False):
         if s.kind == "assign" and s.lhs.kind == "var":
             self.assign_count[s.lhs.op] = self.assign_count.get(s.lhs.op, 0) + 1
-            if id(s) not in self.dead:        # never executed: no candidate value
+            if in_loop:
+                self.seq_vars.add(s.lhs.op)   # assigned in a sequential loop: no static value set
+            elif id(s) not in self.dead:      # never executed: no candidate value
                 self.int_assigns.setdefault(s.lhs.op, []).append(s.rhs)
         for c in ks.children(s):
-            self.count_assigns(c)
+            self.count_assigns(c, in_loop or s.kind == "for")
+        if s.kind == "assign" and s.lhs.kind == "var" and s.lhs.op in self.seq_vars:
+            self.int_assigns.pop(s.lhs.op, None)
+
+    @staticmethod
+    def assigned_in(s: ks.Stmt) -> set:
+        out = set()
+        if s.kind == "assign" and s.lhs.kind == "var":
+            out.add(s.lhs.op)
+        for c in ks.children(s):
+            out |= _Lowerer.assigned_in(c)
+        return out
 
     # -- guards the loop bounds decide ---------------------------------------
     #
@@ -257,6 +271,11 @@ class _Lowerer:
                 env[s.lhs.op] = v
             else:
                 env.pop(s.lhs.op, None)
+        elif k == "for":
+            # a sequential inner loop: every scalar it assigns has no single
+            # linear value afterwards (and none inside: the body repeats)
+            for name in self.assigned_in(s):
+                env.pop(name, None)
         elif k == "if":
             if self.always_false(s.cond, env):
                 self.mark_dead(s.then_s, out)
@@ -566,7 +585,19 @@ class _Lowerer:
             out.append(f"{pad}(void){self.call(s.call)};")
             return
         if k == "for":
-            raise LowerError("sequential loops inside a region body are not supported yet")
+            # a sequential loop inside the per-point body (an unmarked inner
+            # loop: matmul's k, a scan): the thread runs it as written; its
+            # variable is never a static subscript, so loads indexed by it are
+            # dynamic (ldx) and its stores conditional (not must-write)
+            if s.init is not None:
+                self.st(s.init, ind, out)
+            c, _ = self.ex(s.cond) if s.cond is not None else ("1", "int")
+            out.append(f"{pad}while ({c}) {{")
+            self.st(s.body, ind + 1, out)
+            if s.step is not None:
+                self.st(s.step, ind + 1, out)
+            out.append(f"{pad}}}")
+            return
         raise LowerError(f"statement kind {k}")
 
     # -- if-conversion of store-symmetric branches
@@ -884,21 +915,29 @@ class _Lowerer:
         self.count_assigns(body_stmt)
         # function-level locals other than loop vars
         pre: List[str] = []
-        for s in self.fn.body.stmts:
-            if s.kind == "decl":
-                for name, dims, init in s.names:
-                    if name in self.loop_vars:
-                        continue
-                    if dims:
-                        raise LowerError("local arrays are not supported")
-                    self.types[name] = s.ty
-                    ty = "int" if s.ty == "int" else self.real()
-                    pre.append(f"    {ty} {name};")
-            elif s.kind == "for":
-                if s is not self.region.loops[0]:
-                    raise LowerError("only one loop nest per function is supported")
-            elif s.kind != "empty":
-                raise LowerError("statements outside the loop nest are not supported")
+
+        def fn_level(stmts):
+            for s in stmts:
+                if s.kind == "decl":
+                    for name, dims, init in s.names:
+                        if name in self.loop_vars:
+                            continue
+                        if dims:
+                            raise LowerError("local arrays are not supported")
+                        self.types[name] = s.ty
+                        ty = "int" if s.ty == "int" else self.real()
+                        pre.append(f"    {ty} {name};")
+                elif s.kind == "for":
+                    if s is not self.region.loops[0]:
+                        raise LowerError("only one loop nest per function is supported")
+                elif s.kind == "block":
+                    fn_level(s.stmts)          # `#pragma acc parallel { ... }` around the nest
+                elif s.kind != "empty":
+                    raise LowerError("statements outside the loop nest are not supported")
+        fn_level(self.fn.body.stmts)
+        for name in getattr(self, "global_scalars", ()):
+            if self.assign_count.get(name):
+                raise LowerError(f"the region assigns the global scalar '{name}' (a reduction): not offloaded")
         bounds = self.loop_bounds()
         self.pre = pre
         out: List[str] = list(pre)
@@ -913,12 +952,31 @@ class _Lowerer:
                        self.static_refs, self.static_stores)
 
 
+def global_params(mod: ks.Module) -> List[ks.Param]:
+    """File-scope declarations a region reads, as implicit parameters after the
+    function's own (the caller passes the globals' storage / values)."""
+    out = []
+    for s in mod.globals:
+        if s.kind == "decl":
+            for name, dims, init in s.names:
+                out.append(ks.Param(s.ty, name, list(dims)))
+    return out
+
+
+def region_params(mod: ks.Module, fn: ks.Function) -> List[ks.Param]:
+    own = {p.name for p in fn.params}
+    return list(fn.params) + [p for p in global_params(mod) if p.name not in own]
+
+
 def lower_text(text: str, function: str, fma: bool, f32: bool = False, ifconv: bool = True,
                plain: bool = False) -> Lowered:
     mod = ks.parse(text)
     for reg in ks.find_regions(mod):
         if reg.function.name == function:
-            return _Lowerer(reg.function, reg, fma, f32, ifconv, plain).run()
+            fn = ks.Function(reg.function.name, region_params(mod, reg.function), reg.function.body)
+            low = _Lowerer(fn, reg, fma, f32, ifconv, plain)
+            low.global_scalars = {p.name for p in global_params(mod) if not p.dims}
+            return low.run()
     raise LowerError(f"no region in function {function}")
 
 

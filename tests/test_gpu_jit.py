@@ -1,5 +1,6 @@
-"""The B200 wrapper hand-off end to end: a user program (tests/jit/main.c)
-calling a nest file (tests/jit/heat.c) compiled through
+"""The B200 wrapper hand-off end to end: user programs (tests/jit/main*.c)
+calling nest files (tests/jit/heat.c: parameter arrays; matmul_g.c: file-scope
+arrays, a sequential inner reduction loop, a branch) compiled through
 `acs-satcc --backend b200 -- gcc ...` runs the nest on the GPU and prints
 the same bits as the program compiled for the CPU (original and CSE forms:
 bit-exact; the saturated form within the reference comparator rule)."""
@@ -22,16 +23,20 @@ def run(exe):
     return h, float(v)
 
 
+PROGRAMS = {"heat": ("main.c", "heat.c"),               # parameters, 2-D stencil, 4 calls
+            "matmul": ("main_matmul.c", "matmul_g.c")}    # file-scope arrays, inner reduction loop, branch
+
+
+@pytest.mark.parametrize("prog", sorted(PROGRAMS))
 @pytest.mark.parametrize("variant", ["original", "cse", "accsat"])
-def test_wrapped_program_runs_on_the_b200(variant):
-    out = os.path.join(ROOT, "build", f"heat_{variant.replace('+', '_')}")
-    cpu = os.path.join(ROOT, "build", "heat_cpu")
+def test_wrapped_program_runs_on_the_b200(prog, variant):
+    main, nest = (os.path.join(J, f) for f in PROGRAMS[prog])
+    out = os.path.join(ROOT, "build", f"{prog}_{variant.replace('+', '_')}")
+    cpu = os.path.join(ROOT, "build", f"{prog}_cpu")
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    subprocess.run(["gcc", "-O2", "-ffp-contract=off", os.path.join(J, "main.c"), os.path.join(J, "heat.c"), "-o",
-                    cpu], check=True)
+    subprocess.run(["gcc", "-O2", "-ffp-contract=off", main, nest, "-o", cpu], check=True)
     r = subprocess.run([SATCC, "--backend", "b200", "--variant", variant, "--", "gcc", "-O2", "-ffp-contract=off",
-                        os.path.join(J, "main.c"), os.path.join(J, "heat.c"), "-o", out],
-                       capture_output=True, text=True, timeout=900)
+                        main, nest, "-o", out], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr
     nm = subprocess.run(["nm", "-D", out], capture_output=True, text=True).stdout
     assert "acs_eval_host" in nm                # the nest runs through the backend, not on the CPU
