@@ -530,8 +530,45 @@ def bench_configs(kid, size, dtype, sweeps, configs, reps, warmup=3):
     return out, w
 
 
+# read:write array mix of every nest (smallest integers), for the mix-matched stream peak
+MIX = {"jacobi7": (1, 1), "stream_collide": (1, 1), "calc1": (3, 4), "calc2": (7, 3), "calc3": (3, 2),
+       "ideal_gas": (1, 1), "pdv_predict": (3, 1), "advec_cell_x": (2, 1), "wave4": (3, 1), "z_solve_lhs": (2, 3)}
+
+
+def stream_peaks(mixes, elems=1 << 27, reps=10):
+    """acs_stream_probe: best-of-reps GB/s of a pure R-read / W-write stream
+    (1 GiB per array) for every mix — the copy peak is (1, 1); read-heavy
+    nests can exceed it, write-heavy ones cannot reach it."""
+    import ctypes
+    from paper_2306_13002_b200 import backend
+    L = backend.lib()
+    L.acs_stream_probe.restype = ctypes.c_int
+    L.acs_stream_probe.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
+                                   ctypes.POINTER(ctypes.c_float)]
+    out = {}
+    for r, w in sorted(set(mixes)):
+        g = ctypes.c_float()
+        backend._check(L.acs_stream_probe(r, w, elems, reps, ctypes.byref(g)), "acs_stream_probe")
+        out[(r, w)] = round(g.value, 1)
+    return out
+
+
 def per_kernel_table(peak, reps):
     rows = {}
+    try:
+        mixpk = stream_peaks(list(MIX.values()) + [(1, 1), (1, 0)])
+    except Exception as e:   # report, never hide
+        mixpk = {}
+        rows["stream_probe_error"] = str(e)[:200]
+    if mixpk:
+        # the probe kernel reaches a little less than the driver's copy peak at
+        # 1R:1W; its mix-to-mix shape is what matters, so every mix is scaled
+        # by copy_peak / probe(1R:1W)
+        scale = peak / mixpk[(1, 1)]
+        rows["stream_peaks"] = {"raw_gbs": {f"{r}R:{w}W": v for (r, w), v in sorted(mixpk.items())},
+                                "scale_to_copy_peak": round(scale, 4),
+                                "gbs": {f"{r}R:{w}W": round(v * scale, 1) for (r, w), v in sorted(mixpk.items())}}
+        mixpk = {k: v * scale for k, v in mixpk.items()}
     for kid, size, dtype, sweeps in TABLE:
         fn = kid.split(":")[1]
         row = {"size": size, "dtype": dtype, "sweeps_per_step": sweeps, "reps": reps,
@@ -576,6 +613,11 @@ def per_kernel_table(peak, reps):
             row["bytes_per_point"] = w.bytes_per_point
         except Exception:
             pass
+        mix = MIX.get(fn)
+        if mix and mix in mixpk and "accsat/tuned" in row and "gbs" in row["accsat/tuned"]:
+            row["mix"] = f"{mix[0]}R:{mix[1]}W"
+            row["mix_peak_gbs"] = round(mixpk[mix], 1)
+            row["accsat/tuned"]["frac_of_mix_peak"] = round(row["accsat/tuned"]["gbs"] / mixpk[mix], 4)
         rows[fn] = row
     return rows
 

@@ -246,6 +246,11 @@ acs_status acs_ipc_export(const void* dptr, void* handle_out /* 64 bytes */, int
 acs_status acs_ipc_import(const void* handle /* 64 bytes */, int64_t offset, void** dptr_out);
 acs_status acs_ipc_close(void* dptr, int64_t offset);
 
+/* Measurement helper (not the hot path): HBM bandwidth of a pure stream with
+ * `reads` input and `writes` output arrays of `elems` doubles each (best of
+ * `reps`, GB/s) — the peak a nest with the same read:write mix can reach. */
+acs_status acs_stream_probe(int reads, int writes, int64_t elems, int reps, float* gbs_out);
+
 /* Device data utilities (synthetic inputs, layout remaps). */
 typedef enum { ACS_FILL_UNIFORM = 0, ACS_FILL_CONST = 1, ACS_FILL_MASK = 2, ACS_FILL_D3Q19 = 3 } acs_fill_kind;
 /* Fills a (possibly strided) array.  Element at reference flat index f gets

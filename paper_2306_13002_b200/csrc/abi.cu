@@ -721,6 +721,131 @@ acs_status acs_tune(const acs_kernel* k, acs_variant variant, const acs_array* a
     return check_launch("acs_tune");
 }
 
+}  // extern "C"
+
+// ---- measurement helper: HBM stream peak at a given read/write mix ---------
+// R input arrays read and W output arrays written once per element, 16-byte
+// vectors, grid-stride, one wave of resident CTAs: the bandwidth a nest with
+// the same read:write mix could reach (the copy peak is R = W = 1).
+struct StreamPtrs {
+    const double2* in[9];
+    double2* out[6];
+    double* sink;   // reads-only probes: a never-taken store keeps the loads alive
+};
+// each CTA streams contiguous 4 x 256 x 16-byte chunks (grid-strided over
+// chunks), loads of all R arrays issued before any use
+template <int R, int W>
+__global__ void __launch_bounds__(256) stream_rw_kernel(StreamPtrs p, long long n2) {
+    constexpr int U = 4;
+    const long long chunk = (long long)U * blockDim.x;
+    double2 tot = make_double2(0.0, 0.0);
+    for (long long c0 = blockIdx.x * chunk; c0 < n2; c0 += (long long)gridDim.x * chunk) {
+        double2 v[U][R];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const long long i = c0 + u * blockDim.x + threadIdx.x;
+                v[u][r] = i < n2 ? p.in[r][i] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long i = c0 + u * blockDim.x + threadIdx.x;
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                acc.x += v[u][r].x;
+                acc.y += v[u][r].y;
+            }
+            if (i < n2) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) p.out[w][i] = make_double2(acc.x + w, acc.y - w);
+            }
+            tot.x += acc.x;
+            tot.y += acc.y;
+        }
+    }
+    if (W == 0 && tot.x + tot.y == 1.25e300) *p.sink = tot.x;
+}
+template <int R, int W>
+static acs_status stream_launch(const StreamPtrs& p, long long n2, cudaStream_t s) {
+    int dev = 0, sms = 148, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_rw_kernel<R, W>, 256, 0);
+    stream_rw_kernel<R, W><<<sms * (per > 0 ? per : 1), 256, 0, s>>>(p, n2);
+    return ACS_OK;
+}
+template <int R, int W>
+static acs_status stream_dispatch_w(int w, const StreamPtrs& p, long long n2, cudaStream_t s) {
+    if constexpr (W > 6) {
+        return ACS_E_ARG;
+    } else {
+        if (w == W) return stream_launch<R, W>(p, n2, s);
+        return stream_dispatch_w<R, W + 1>(w, p, n2, s);
+    }
+}
+template <int R>
+static acs_status stream_dispatch(int r, int w, const StreamPtrs& p, long long n2, cudaStream_t s) {
+    if constexpr (R > 9) {
+        return ACS_E_ARG;
+    } else {
+        if (r == R) return stream_dispatch_w<R, 0>(w, p, n2, s);
+        return stream_dispatch<R + 1>(r, w, p, n2, s);
+    }
+}
+
+extern "C" {
+
+acs_status acs_stream_probe(int reads, int writes, int64_t elems, int reps, float* gbs_out) {
+    if (reads < 1 || reads > 9 || writes < 0 || writes > 6 || elems < 2 || reps < 1 || !gbs_out) {
+        set_error("acs_stream_probe: reads 1..9, writes 0..6, elems >= 2, reps >= 1");
+        return ACS_E_ARG;
+    }
+    const long long n2 = elems / 2;
+    const size_t bytes = (size_t)n2 * sizeof(double2);
+    StreamPtrs p{};
+    std::vector<void*> bufs;
+    double* sink = nullptr;
+    cudaMalloc(&sink, sizeof(double));
+    p.sink = sink;
+    auto cleanup = [&] {
+        for (void* b : bufs) cudaFree(b);
+        cudaFree(sink);
+    };
+    for (int i = 0; i < reads + writes; ++i) {
+        void* b = nullptr;
+        if (cudaMalloc(&b, bytes) != cudaSuccess) {
+            cleanup();
+            set_error("acs_stream_probe: cudaMalloc failed");
+            return ACS_E_CUDA;
+        }
+        cudaMemset(b, 0, bytes);
+        bufs.push_back(b);
+        if (i < reads) p.in[i] = static_cast<const double2*>(b);
+        else p.out[i - reads] = static_cast<double2*>(b);
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    std::vector<float> t((size_t)reps);
+    acs_status st = stream_dispatch<1>(reads, writes, p, n2, nullptr);   // warm-up
+    for (int i = 0; i < reps && st == ACS_OK; ++i) {
+        cudaEventRecord(e0, nullptr);
+        st = stream_dispatch<1>(reads, writes, p, n2, nullptr);
+        cudaEventRecord(e1, nullptr);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&t[i], e0, e1);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cleanup();
+    if (st != ACS_OK) return st;
+    std::sort(t.begin(), t.end());
+    *gbs_out = (float)((double)bytes * (reads + writes) / (t[0] * 1e-3) / 1e9);   // best of reps, like the copy peak
+    return check_launch("acs_stream_probe");
+}
+
 acs_status acs_fill(const acs_array* a, acs_fill_kind kind, uint64_t seed, double lo, double hi, double p,
                     int64_t flat_offset, void* cuda_stream) {
     StridedDesc d;
