@@ -19,9 +19,10 @@ void register_wave4() {
         fill_march<gen::wave4_f32, float, 0, 64, 8, 64, 8, 3>(e, 1);
         fill_march<gen::wave4_f32, float, 0, 64, 8, 64, 2, 3>(e, 1);
         fill_march<gen::wave4_f32, float, 0, 64, 16, 64, 4, 2>(e, 1);
-        fill_march<gen::wave4_f32, float, 0, 64, 16, 16, 16, 2, 4>(e, 1);
-        fill_march<gen::wave4_f32, float, 0, 64, 16, 16, 16, 1, 4>(e, 1);
         fill_march<gen::wave4_f32, float, 0, 128, 8, 32, 8, 2, 4>(e, 1);
+        fill_march<gen::wave4_f32, float, 0, 64, 8, 64, 2, 4>(e, 1);
+        fill_march<gen::wave4_f32, float, 0, 64, 16, 16, 16, 2, 4>(e, 1);
+        fill_march<gen::wave4_f32, float, 0, 32, 16, 32, 4, 3>(e, 1);
         register_entry(&e);
     }
 }
