@@ -443,9 +443,11 @@ def e2e_host_runner(args, w, k, dist):
     stream = torch.cuda.current_stream()
     # host inputs in the reference layout (generated on device, copied once, untimed)
     dev_rm = nests.device_inputs(w, native=False, kernel=k)
-    host = {n: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for n, t in dev_rm.items()}
+    # 0/1 int masks travel as bytes (the host buffer of D3Q19's flags is uint8)
+    host = {n: torch.empty(t.shape, dtype=torch.uint8 if n == "flags" else t.dtype, pin_memory=True)
+            for n, t in dev_rm.items()}
     for n, t in dev_rm.items():
-        host[n].copy_(t)
+        host[n].copy_(t.to(torch.uint8) if n == "flags" else t)
     del dev_rm
     torch.cuda.synchronize()
     runner = pipeline_exec.HostRunner(k, host, w.spec.range_params, chunks=args.e2e_chunks)

@@ -124,7 +124,11 @@ class HostRunner:
         self.ramp = ramp
         self.reach = reaches(k)
         self.rm = {n: torch.empty(tuple(t.shape), dtype=t.dtype, device="cuda") for n, t in host.items()}
-        self.nat = {n: backend.empty_native(k, n, tuple(t.shape), t.dtype) for n, t in host.items()}
+        # a 0/1 mask the nest declares `int` may be held on the host as bytes
+        # (D3Q19 flags: 17 MB instead of 68 MB over PCIe per call); the device
+        # copy the kernel reads is int32, widened by the remap (acs_copy u8 -> i32)
+        self.nat = {n: backend.empty_native(k, n, tuple(t.shape), torch.int32 if t.dtype == torch.uint8 else t.dtype)
+                    for n, t in host.items()}
         self.s_h2d, self.s_cmp, self.s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
         self.s_d2h2 = torch.cuda.Stream()      # second download stream (a second copy engine)
         self.split_d2h = False

@@ -345,3 +345,22 @@ def test_empty_iteration_space_is_a_noop(kid, which):
 
 # Full BASELINE sizes (every form, naive + tuned slots, wave4 1024^3, zsolve 256^3,
 # the Jacobi graph step, the slab path, the e2e path) and edge values: tests/test_gpu_fullsize.py
+
+
+def test_host_runner_byte_mask():
+    """D3Q19's 0/1 flags held on the host as bytes (the kernel reads int32):
+    the host-buffer call widens them on the device, same result."""
+    torch = _torch()
+    from paper_2306_13002_b200 import pipeline_exec
+    kid = "d3q19.c:stream_collide:0"
+    spec = nests.kernel(kid)
+    w = nests.workload(kid, (9, 7, 20))
+    ins = nests.make_inputs(w)
+    want = {n: a.copy() for n, a in ins.items()}
+    oracle_cpu.run(spec, want, w.scalars, "accsat", fma=True)
+    host = {n: torch.from_numpy(a.astype(np.uint8) if n == "flags" else a.copy()).pin_memory() for n, a in ins.items()}
+    r = pipeline_exec.HostRunner(backend.Kernel.lookup(kid), host, spec.range_params, chunks=3)
+    r.run(dict(w.scalars), "accsat")
+    torch.cuda.synchronize()
+    assert bitwise_equal(host["dst"].numpy(), want["dst"])
+    assert r.bytes_per_call()[0] < sum(a.nbytes for a in ins.values())
