@@ -586,6 +586,10 @@ def per_kernel_table(peak, reps):
         keys = [("original", "naive", "original/naive"), ("original", slots.get("original"), "original/tuned"),
                 ("original-nvcc", "naive", "original-nvcc/naive"), ("accsat", "naive", "accsat/naive"),
                 ("accsat", slots.get("accsat"), "accsat/tuned")]
+        if fn == "jacobi7":
+            # temporal blocking (two sweeps per launch, kernels/tblock.cuh): algorithmic
+            # bytes as for every form (16 B/point/sweep); DRAM bytes are about half
+            keys.append(("accsat", "tb2", "accsat/tb2"))
         keys = [kk for kk in keys if kk[1] is not None]
         try:
             res, w = bench_configs(kid, size, dtype, sweeps, [(v, s) for v, s, _ in keys], reps)

@@ -228,6 +228,16 @@ acs_status acs_wait(const uint64_t* flag_a, const uint64_t* flag_b, uint64_t val
 acs_status acs_signal_ctr(uint64_t* flag_a, uint64_t* flag_b, uint64_t* counter, void* cuda_stream);
 acs_status acs_wait_ctr(const uint64_t* flag_a, const uint64_t* flag_b, const uint64_t* counter, int timeout_ms,
                         void* cuda_stream);
+/* Time stepping of a ping-pong nest (jacobi7: A0 <-> Anext): `nsteps` steps
+ * of the nest's time loop, each step reading the buffer the previous one
+ * wrote (step 0 reads the array the nest reads).  blocked != 0 runs two steps
+ * per launch where a temporal-blocking skeleton is registered (one pass over
+ * HBM per two steps, bit-identical results); otherwise one DEFAULT launch per
+ * step.  *latest = the index in `arrays` of the buffer holding the newest
+ * field (with blocking the other buffer does not hold the previous step). */
+acs_status acs_launch_steps(const acs_kernel* k, acs_variant variant, const acs_array* arrays, int n_arrays,
+                            const acs_scalar* scalars, int n_scalars, int nsteps, int blocked, void* cuda_stream,
+                            int* latest);
 /* eval_region for HOST arrays (row-major, the reference layout; `data` =
  * host pointers): uploads every array, runs the whole nest with the DEFAULT
  * schedule, downloads every array the nest stores, synchronously.  The call a

@@ -197,6 +197,22 @@ class Kernel:
         _check(lib().acs_launch(self.handle, VARIANTS[variant], sched, descs, len(arrays), sc,
                                 len(scalars), _stream_handle(stream)), f"acs_launch({self.kernel_id}, {variant})")
 
+    def launch_steps(self, arrays: Dict[str, object], scalars: Dict[str, float], variant: str = "accsat",
+                     nsteps: int = 1, blocked: bool = True, stream=None) -> str:
+        """acs_launch_steps: `nsteps` steps of a ping-pong nest's time loop
+        (two per launch with temporal blocking where registered); returns the
+        name of the array holding the newest field."""
+        names = list(arrays)
+        descs, sc = self._pack(arrays, scalars)
+        latest = ctypes.c_int(-1)
+        f = lib().acs_launch_steps
+        f.restype = ctypes.c_int
+        f.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(AcsArray), ctypes.c_int, ctypes.POINTER(AcsScalar),
+                      ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]
+        _check(f(self.handle, VARIANTS[variant], descs, len(names), sc, len(scalars), nsteps, 1 if blocked else 0,
+                 _stream_handle(stream), ctypes.byref(latest)), f"acs_launch_steps({self.kernel_id})")
+        return names[latest.value]
+
     def tune(self, arrays, scalars, variant: str = "accsat", reps: int = 3, stream=None):
         """acs_tune: times every registered schedule slot on these arrays and
         makes the fastest the default for this variant.  Returns

@@ -490,6 +490,62 @@ acs_status acs_wait(const uint64_t* flag_a, const uint64_t* flag_b, uint64_t val
     return check_launch("acs_wait");
 }
 
+acs_status acs_launch_steps(const acs_kernel* k, acs_variant variant, const acs_array* arrays, int n_arrays,
+                            const acs_scalar* scalars, int n_scalars, int nsteps, int blocked, void* cuda_stream,
+                            int* latest) {
+    if (!k || !arrays || n_arrays != 2 || nsteps < 0 || !latest || (int)variant < 0 || (int)variant > 4) {
+        set_error("acs_launch_steps: a ping-pong nest (two arrays), nsteps >= 0, a latest out-parameter");
+        return ACS_E_ARG;
+    }
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    if (e->arrays.size() != 2) {
+        set_error(e->kernel_id + ": acs_launch_steps needs a two-array ping-pong nest");
+        return ACS_E_ARG;
+    }
+    // the array each step reads (loaded, never stored) and the one it writes
+    int rd = -1;
+    for (int a = 0; a < 2; ++a)
+        if (e->reach[a].loaded && !e->reach[a].stored) rd = a;
+    if (rd < 0 || !e->reach[1 - rd].stored) {
+        set_error(e->kernel_id + ": not a ping-pong nest (one array read, the other written)");
+        return ACS_E_ARG;
+    }
+    int ir = -1, iw = -1;   // positions in `arrays`
+    for (int i = 0; i < 2; ++i) {
+        if (arrays[i].name && e->arrays[rd] == arrays[i].name) ir = i;
+        if (arrays[i].name && e->arrays[1 - rd] == arrays[i].name) iw = i;
+    }
+    if (ir < 0 || iw < 0) {
+        set_error(e->kernel_id + ": acs_launch_steps: arrays must be named " + e->arrays[0] + ", " + e->arrays[1]);
+        return ACS_E_ARG;
+    }
+    const int prec = precision_of(arrays, n_arrays);
+    acs_array cur = arrays[ir], oth = arrays[iw];
+    const cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    int left = nsteps;
+    while (left > 0) {
+        acs_array step[2];
+        step[ir] = cur;
+        step[iw] = oth;
+        step[ir].name = arrays[ir].name;
+        step[iw].name = arrays[iw].name;
+        acs_status st;
+        LaunchFn tb = blocked ? e->tb2[prec][variant] : nullptr;
+        if (tb && left >= 2) {
+            LaunchReq r{step, 2, scalars, n_scalars, s};
+            st = tb(r);
+            left -= 2;
+        } else {
+            st = launch_impl(k, variant, ACS_SCHED_DEFAULT, step, 2, scalars, n_scalars, nullptr, cuda_stream);
+            left -= 1;
+        }
+        if (st != ACS_OK) return st;
+        std::swap(cur.data, oth.data);   // the written buffer is read next
+    }
+    *latest = cur.data == arrays[ir].data ? ir : iw;
+    return ACS_OK;
+}
+
 acs_status acs_eval_host(const acs_kernel* k, acs_variant variant, const acs_array* host, int n_arrays,
                          const acs_scalar* scalars, int n_scalars) {
     if (!k || (n_arrays > 0 && !host) || (n_scalars > 0 && !scalars)) {

@@ -56,6 +56,9 @@ struct Entry {
     int static_loads[5] = {0, 0, 0, 0, 0};
     int fma_count[5] = {0, 0, 0, 0, 0};
     LaunchFn launch[2][6][kMaxSched] = {};   // variant 5 = ACS_ORIGINAL_NVCC (naive slot only)
+    LaunchFn tb2[2][5] = {};                 // two time steps per launch (kernels/tblock.cuh), ping-pong nests
+    std::string tb2_name[2];
+    int tb2_read = -1;                       // registry index of the array a tb2 step reads
     std::string sched_name[2][kMaxSched];
     int n_sched[2] = {1, 1};     // slot 0 (naive) always present once registered
     int best[2][6] = {};         // preferred slot per (precision, variant); acs_tune updates it

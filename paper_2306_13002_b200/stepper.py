@@ -35,6 +35,12 @@ class Stepper:
         self.k.launch({p: self.arrays[b] for p, b in roles.items()}, self.scalars, self.variant, self.schedule,
                       stream)
 
+    @property
+    def blocked(self) -> bool:
+        """schedule "tb2": the whole step as acs_launch_steps with temporal
+        blocking (two sweeps per launch, kernels/tblock.cuh)."""
+        return self.schedule == "tb2"
+
     def capture(self, stream=None) -> None:
         """One CUDA graph of a step.  Needs `sweeps` to be a multiple of the
         rotation period (the graph's buffers are fixed) and a step count of
@@ -49,11 +55,24 @@ class Stepper:
         cs = torch.cuda.Stream()
         cs.wait_stream(stream)
         with torch.cuda.graph(g, stream=cs):
-            for t in range(self.sweeps):
-                self._launch(t, cs)
+            if self.blocked:
+                self._steps(cs)
+            else:
+                for t in range(self.sweeps):
+                    self._launch(t, cs)
         stream.wait_stream(cs)
         torch.cuda.synchronize()
         self.graph = g
+
+    def _steps(self, stream) -> None:
+        if self.sweeps % 4:
+            raise ValueError("tb2 steps: a multiple of 4 sweeps keeps the newest field in the ping-pong's buffer")
+        names = self.names
+        latest = self.k.launch_steps({n: self.arrays[n] for n in names}, self.scalars, self.variant, self.sweeps,
+                                     True, stream)
+        want = nests.role_buffers(self.nest, names, self.sweeps)[nests.ROTATIONS[self.nest][0][0]]
+        if latest != want:
+            raise RuntimeError(f"tb2 steps left the newest field in {latest}, the time loop expects {want}")
 
     def step(self, stream=None) -> None:
         torch = self.torch
@@ -61,6 +80,10 @@ class Stepper:
         if self.graph is not None:
             with torch.cuda.stream(stream):
                 self.graph.replay()
+            self.t += self.sweeps
+            return
+        if self.blocked:
+            self._steps(stream)
             self.t += self.sweeps
             return
         for _ in range(self.sweeps):

@@ -364,3 +364,27 @@ def test_host_runner_byte_mask():
     torch.cuda.synchronize()
     assert bitwise_equal(host["dst"].numpy(), want["dst"])
     assert r.bytes_per_call()[0] < sum(a.nbytes for a in ins.values())
+
+
+@pytest.mark.parametrize("size", [(6, 7, 19), (21, 9, 70), (33, 47, 130)])
+@pytest.mark.parametrize("nsteps", [1, 2, 5, 8])
+@pytest.mark.parametrize("variant", ["original", "accsat"])
+def test_temporal_blocking_equals_step_by_step(size, nsteps, variant):
+    """acs_launch_steps with temporal blocking (two Jacobi sweeps per launch,
+    the step-1 field held in shared memory) gives the newest field of the
+    ping-pong time loop bit for bit (odd counts end with one plain step)."""
+    torch = _torch()
+    kid = "jacobi7.c:jacobi7:0"
+    spec = nests.kernel(kid)
+    w = nests.workload(kid, size)
+    ins = nests.make_inputs(w)
+    g = {n: a.copy() for n, a in ins.items()}
+    for t in range(nsteps):
+        roles = nests.role_buffers(spec.nest, list(g), t)
+        oracle_cpu.run(spec, {p: g[b] for p, b in roles.items()}, w.scalars, variant, fma=variant in SAT)
+    newest = nests.role_buffers(spec.nest, list(g), nsteps)["A0"]
+    k = backend.Kernel.lookup(kid)
+    dev = {n: to_device(k, n, a) for n, a in ins.items()}
+    latest = k.launch_steps(dev, dict(w.scalars), variant, nsteps, blocked=True)
+    got = to_host(dev[latest])
+    assert bitwise_equal(got, g[newest]), f"{size} x{nsteps}"
