@@ -619,6 +619,35 @@ struct FastState {
     // k-column register queue: a ring array whose column the body reads in its
     // top plane and in at least one lower plane — the lower planes' values were
     // read as the top plane of earlier steps and stay in registers
+    // lowest march plane of array a the body reads from SHARED memory in form
+    // `form`: every plane for unqueued arrays; for queued ones the planes of
+    // their non-column loads (rows off the thread's own column) and the top
+    // plane that feeds the queue — lower column planes live in registers
+    static constexpr int smem_lo(int a, int form) {
+        const int mp = P::march_pos(a);
+        if (!queued(a, form)) return NS::ld_lo(a, mp);
+        int lo = NS::ld_hi(a, mp);
+        for (int r = 0; r < NS::NROW; ++r) {
+            if (NS::row_arr(r) != a || !((NS::row_forms(r) >> form) & 1)) continue;
+            bool col = NS::row_xlo(r) == 0 && NS::row_xhi(r) == 0;
+            for (int p = 0; p < NS::ndim(a); ++p)
+                if (p != mp && NS::row_off(r, p) != 0) col = false;
+            if (!col && NS::row_off(r, mp) < lo) lo = NS::row_off(r, mp);
+        }
+        return lo;
+    }
+    // ring planes the hoisted path needs resident: the deepest shared-memory
+    // reach of any staged array (the queue prologue still reads the full span
+    // once, at step 0, so the ring never holds fewer bundles than the span)
+    static constexpr int smem_span(int form) {
+        int m = 1;
+        for (int a = 0; a < NS::NARR; ++a)
+            if (P::on_ring(a)) {
+                const int sp = NS::ld_hi(a, P::march_pos(a)) - smem_lo(a, form) + 1;
+                if (sp > m) m = sp;
+            }
+        return m;
+    }
     static constexpr bool queued(int a, int form) {
         if (!P::on_ring(a) || P::span(a) < 2 || NS::is_int(a)) return false;
         const int mp = P::march_pos(a);
@@ -745,7 +774,7 @@ __device__ __forceinline__ void fast_points(MM& m, const FS& fs, Q q, const Kern
 
 // prologue of the k-column queue: the lower planes of step 0 from the ring
 template <class NS, class P, class FS, int FORM, int NPX, int NPY, int BX, int A, class T, class Q>
-__device__ __forceinline__ void fast_queue_fill(const unsigned char* ring, const FS& fs, Q q) {
+__device__ __forceinline__ void fast_queue_fill(const unsigned char* ring, const FS& fs, Q q, int b) {
     if constexpr (A < NS::NARR) {
         if constexpr (FS::queued(A, FORM)) {
             constexpr int mp = P::march_pos(A);
@@ -765,10 +794,11 @@ __device__ __forceinline__ void fast_queue_fill(const unsigned char* ring, const
                 }
 #pragma unroll
                 for (int i = 0; i < P::span(A) - 1; ++i)
-                    q[A][I][i] = *reinterpret_cast<const T*>(ring + fs.plane[A][i] + c * (int)sizeof(T));
+                    if (P::maxspan() - P::span(A) + i == b)   // plane i of array A arrives in bundle b
+                        q[A][I][i] = *reinterpret_cast<const T*>(ring + fs.plane[A][i] + c * (int)sizeof(T));
             }
         }
-        fast_queue_fill<NS, P, FS, FORM, NPX, NPY, BX, A + 1, T>(ring, fs, q);
+        fast_queue_fill<NS, P, FS, FORM, NPX, NPY, BX, A + 1, T>(ring, fs, q, b);
     }
 }
 
@@ -891,6 +921,21 @@ __device__ __forceinline__ void win_rows(M& m, const T* win, bool vec_ok, const 
     }
 }
 
+// ring depth of a march kernel: span + PF bundles; on the hoisted 3-D path the
+// k-column queue keeps the lower column planes in registers, so only the
+// planes read from shared memory count (the queue prologue consumes the lower
+// bundles one by one and recycles their slots).  wave4 u: 5 + PF -> 3 + PF.
+template <class NS, class T, int LAYOUT, int TX, int TY, int RX, int PF, int FORM>
+constexpr int march_ring_depth() {
+    using P = MarchPlan<NS, T, LAYOUT, TX, TY, RX>;
+    constexpr int MS = P::maxspan();
+    if constexpr (RX == 1 && NS::NLOOP == 3) {
+        return FastState<NS, T, P, MS>::smem_span(FORM) + PF;
+    } else {
+        return MS + PF;
+    }
+}
+
 template <class NS, class T, int FORM, int LAYOUT, int TX, int TY, int BX, int BY, int PF, int RX = 1>
 __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ KernelArgs<NS> args,
                                                        const __grid_constant__ TmaMaps<NS> maps, int kchunk) {
@@ -898,7 +943,8 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
     static_assert(RX == 1 || TX == BX * RX, "register windows: one RX group of adjacent points per thread");
     using P = MarchPlan<NS, T, LAYOUT, TX, TY, RX>;
     using M = MarchMem<NS, T, LAYOUT, TX, TY, PF, RX>;
-    constexpr int D = M::D;
+    constexpr int D = march_ring_depth<NS, T, LAYOUT, TX, TY, RX, PF, FORM>();
+    static_assert(RX == 1 && NS::NLOOP == 3 || D == M::D, "generic path: the ring depth MarchMem assumes");
     constexpr int MS = P::maxspan();
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* ring = smem;
@@ -915,6 +961,13 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
     const int ke = min(kb + kchunk, args.hi[0]);
     const int ns = ke - kb;
     const int nb = ns + MS - 1;   // bundles this chunk consumes
+    // hoisted-addressing path (3-D nests, one point per thread column); 2-D row
+    // strips are DRAM-bound already and keep the generic path (smaller code)
+    constexpr bool FAST = RX == 1 && NS::NLOOP == 3;
+    using FS = FastState<NS, T, P, MS>;
+    // planes of the ring the FAST path reads after the queue prologue: bundle
+    // s + MS - SS is the oldest step s needs (SS == MS without a queue)
+    constexpr int SS = FAST ? FS::smem_span(FORM) : MS;
 
     if (tid == 0) {
         for (int s = 0; s <= D; ++s) mbar_init(&bars[s], 1);
@@ -926,7 +979,7 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
             mbar_expect_tx(&bars[D], P::static_tx());
             march_issue<P, NS, 0>(nullptr, maps, &bars[D], 0, orgx + maps.adjx, orgy, true, stat);
         }
-        for (int B = 0; B < D - 1 && B < nb; ++B) {
+        for (int B = 0; B < (FAST ? D : D - 1) && B < nb; ++B) {
             mbar_expect_tx(&bars[B % D], P::slot_tx());
             march_issue<P, NS, 0>(ring + (B % D) * P::slot_bytes(), maps, &bars[B % D], kb + B - (MS - 1), orgx + maps.adjx,
                                   orgy, false, stat);
@@ -934,8 +987,10 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
     }
     if constexpr (P::static_tx() > 0) mbar_wait(&bars[D], 0);
     // TMA transfers complete in any order: step 0 needs bundles 0 .. MS-1, the
-    // loop below waits only for the newest bundle of each step.
-    for (int B = 0; B < MS - 1 && B < nb; ++B) mbar_wait(&bars[B % D], 0);
+    // loop below waits only for the newest bundle of each step (the FAST path
+    // waits for them one by one in its queue prologue)
+    if constexpr (!FAST)
+        for (int B = 0; B < MS - 1 && B < nb; ++B) mbar_wait(&bars[B % D], 0);
 
     int pt[NS::NLOOP];
     M m{NaiveMem<NS, T, false>{args, pt}, ring, stat, 0, tx, ty, 0, orgx, orgy, {}};
@@ -964,10 +1019,6 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
 
     T win[WP::usable() ? WP::total() : 1];   // register windows, carried across steps (queue)
     // RX == 1: the thread's per-array box offsets, global pointers and in-domain points (march-invariant)
-    // hoisted-addressing path (3-D nests, one point per thread column); 2-D row
-    // strips are DRAM-bound already and keep the generic path (smaller code)
-    constexpr bool FAST = RX == 1 && NS::NLOOP == 3;
-    using FS = FastState<NS, T, P, MS>;
     constexpr int NPX = TX / BX, NPY = TY / BY, NPTS = NPX * NPY;
     FS fs;
     unsigned toff[NS::NARR];
@@ -1029,21 +1080,43 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
                 const int x = orgx + tx + rx * BX, y = orgy + ly0 + ry;
                 inb[ry * NPX + rx] = x < args.hi[P::X] && x >= xlo0 && (NS::NLOOP < 3 || y < args.hi[1]);
             }
-        if (ns > 0) {                               // step 0's lower planes are in (waited above)
+        if (ns > 0) {
+            // queue prologue, bundle by bundle: the lower column planes of step 0
+            // go to registers; a bundle no step reads from shared memory
+            // (b < MS - SS) frees its slot for the bundle D further on
             set_planes((MS - 1) % D);
-            fast_queue_fill<NS, P, FS, FORM, NPX, NPY, BX, 0, T>(ring, fs, q);
+            for (int b = 0; b < MS - 1; ++b) {
+                mbar_wait(&bars[b % D], (uint32_t)((b / D) & 1));
+                fast_queue_fill<NS, P, FS, FORM, NPX, NPY, BX, 0, T>(ring, fs, q, b);
+                if (b < MS - SS) {
+                    __syncthreads();
+                    if (tid == 0 && b + D < nb) {
+                        fence_proxy_async();
+                        mbar_expect_tx(&bars[b % D], P::slot_tx());
+                        march_issue<P, NS, 0>(ring + (b % D) * P::slot_bytes(), maps, &bars[b % D],
+                                              kb + b + D - (MS - 1), orgx + maps.adjx, orgy, false, stat);
+                    }
+                }
+            }
         }
     }
     if constexpr (FAST) {
-        // ring bookkeeping carried across steps (no division per step)
-        int newest = (MS - 1) % D, phase = ((MS - 1) / D) & 1, islot = (D - 1) % D;
+        // ring bookkeeping carried across steps (no division per step).  Step s
+        // (s >= 1) frees bundle s-1+MS-SS (the oldest step s-1 read) and
+        // issues bundle s-1+MS-SS+D into its slot; step 0's were issued above.
+        int newest = (MS - 1) % D, phase = ((MS - 1) / D) & 1, islot = (MS - SS) % D;
+        int ib = MS - SS + D;                       // next bundle to issue
         auto step = [&](int s) __attribute__((always_inline)) {
             __syncthreads();   // every thread is done with step s-1: its oldest slot is free
-            if (tid == 0 && s + D - 1 < nb) {
-                fence_proxy_async();
-                mbar_expect_tx(&bars[islot], P::slot_tx());
-                march_issue<P, NS, 0>(ring + islot * P::slot_bytes(), maps, &bars[islot], kb + s + D - 1 - (MS - 1),
-                                      orgx + maps.adjx, orgy, false, stat);
+            if (s > 0) {
+                if (tid == 0 && ib < nb) {
+                    fence_proxy_async();
+                    mbar_expect_tx(&bars[islot], P::slot_tx());
+                    march_issue<P, NS, 0>(ring + islot * P::slot_bytes(), maps, &bars[islot], kb + ib - (MS - 1),
+                                          orgx + maps.adjx, orgy, false, stat);
+                }
+                ++ib;
+                islot = islot + 1 == D ? 0 : islot + 1;
             }
             mbar_wait(&bars[newest], (uint32_t)phase);
             pt[0] = kb + s;
@@ -1056,7 +1129,6 @@ __global__ void __launch_bounds__(BX* BY) march_kernel(const __grid_constant__ K
 #pragma unroll
             for (int a = 0; a < NS::NARR; ++a)
                 if (FS::needs_gp(a, FORM)) fs.gp[a] += fs.gstep[a];
-            islot = islot + 1 == D ? 0 : islot + 1;
             if (++newest == D) {
                 newest = 0;
                 phase ^= 1;
@@ -1221,7 +1293,7 @@ acs_status launch_march(const LaunchReq& r) {
         }
         return launch_naive<NS, T, FORM>(r);
     }
-    constexpr int D = P::maxspan() + PF;
+    constexpr int D = march_ring_depth<NS, T, LAYOUT, TX, TY, RX, PF, FORM>();
     constexpr int smem = D * P::slot_bytes() + P::static_bytes() + (D + 1) * 8;
     auto kern = march_kernel<NS, T, FORM, LAYOUT, TX, TY, BX, BY, PF, RX>;
     static std::atomic<unsigned long long> attr_done{0};
