@@ -172,7 +172,8 @@ acs_status acs_launch(const acs_kernel* k, acs_variant variant, acs_schedule sch
 const char* acs_kernel_schedule_name(const acs_kernel* k, int precision, int slot);
 
 /* Autotuning: times every registered slot for this variant on these arrays
- * (each `reps` launches after one warm-up, the median launch time; the arrays are updated as by
+ * (one warm-up each, then `reps` rounds launching every slot once — interleaved, so clock drift
+ * hits all slots alike — and the median launch time per slot; the arrays are updated as by
  * repeated launches), records the fastest as what ACS_SCHED_DEFAULT /
  * ACS_SCHED_TILED use for this (kernel, precision, variant) from now on, and
  * returns it.  ms_per_launch[slot] (optional, kMaxSched=8 entries) receives

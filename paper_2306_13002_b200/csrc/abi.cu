@@ -724,50 +724,51 @@ acs_status acs_tune(const acs_kernel* k, acs_variant variant, const acs_array* a
     const int prec = precision_of(arrays, n_arrays);
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     LaunchReq r{arrays, n_arrays, scalars, n_scalars, s, nullptr, true};
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    float best = 1e30f;
-    int bslot = -1;
+    // candidates: every registered slot that takes this layout (one warm-up
+    // launch each: TMA attributes, code loading)
+    std::vector<int> cand;
     for (int slot = 0; slot < kMaxSched; ++slot) {
         if (ms_per_launch) ms_per_launch[slot] = -1.0f;
         LaunchFn fn = e->launch[prec][variant][slot];
         if (!fn) continue;
-        acs_status st = fn(r);   // warm-up (and TMA attribute setup)
+        const acs_status st = fn(r);
         if (st == ACS_E_LAYOUT) continue;   // this skeleton cannot take the layout: not a candidate
-        if (st != ACS_OK) {
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
-            return st;
+        if (st != ACS_OK) return st;
+        cand.push_back(slot);
+    }
+    if (cand.empty()) {
+        set_error("acs_tune: no registered schedule");
+        return ACS_E_NO_KERNEL;
+    }
+    // repetitions interleaved across the candidates (a clock / power-cap drift
+    // over the tuning run hits every slot alike), per-launch events, median
+    const size_t nc = cand.size();
+    std::vector<cudaEvent_t> ev(nc * (size_t)reps * 2);
+    for (auto& x : ev) cudaEventCreate(&x);
+    for (int i = 0; i < reps; ++i)
+        for (size_t c = 0; c < nc; ++c) {
+            cudaEventRecord(ev[(c * reps + i) * 2], s);
+            e->launch[prec][variant][cand[c]](r);
+            cudaEventRecord(ev[(c * reps + i) * 2 + 1], s);
         }
-        // per-launch events, median: one slow launch (clock or power-cap
-        // transient) must not decide the slot
-        std::vector<cudaEvent_t> ev((size_t)reps + 1);
-        for (auto& x : ev) cudaEventCreate(&x);
-        cudaEventRecord(ev[0], s);
-        for (int i = 0; i < reps; ++i) {
-            fn(r);
-            cudaEventRecord(ev[i + 1], s);
-        }
-        if (cudaEventSynchronize(ev[reps]) != cudaSuccess) {
-            for (auto& x : ev) cudaEventDestroy(x);
-            cudaEventDestroy(e0);
-            cudaEventDestroy(e1);
-            return check_launch("acs_tune");
-        }
-        std::vector<float> t((size_t)reps);
-        for (int i = 0; i < reps; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+    if (cudaEventSynchronize(ev.back()) != cudaSuccess) {
         for (auto& x : ev) cudaEventDestroy(x);
+        return check_launch("acs_tune");
+    }
+    float best = 1e30f;
+    int bslot = -1;
+    for (size_t c = 0; c < nc; ++c) {
+        std::vector<float> t((size_t)reps);
+        for (int i = 0; i < reps; ++i) cudaEventElapsedTime(&t[i], ev[(c * reps + i) * 2], ev[(c * reps + i) * 2 + 1]);
         std::sort(t.begin(), t.end());
         const float ms = reps % 2 ? t[reps / 2] : 0.5f * (t[reps / 2 - 1] + t[reps / 2]);
-        if (ms_per_launch) ms_per_launch[slot] = ms;
+        if (ms_per_launch) ms_per_launch[cand[c]] = ms;
         if (ms < best) {
             best = ms;
-            bslot = slot;
+            bslot = cand[c];
         }
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    for (auto& x : ev) cudaEventDestroy(x);
     if (bslot < 0) {
         set_error("acs_tune: no registered schedule");
         return ACS_E_NO_KERNEL;
