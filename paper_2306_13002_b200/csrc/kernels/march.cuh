@@ -740,12 +740,21 @@ struct FastPt {
     __device__ __forceinline__ void st(elem_t<ARR> v) const {
         if (!act) return;
         if constexpr (FS::stored_static(ARR, FORM)) {
-            if (!m.g.a.sh.enabled) {
+            // sharded launch: only planes within reach of a slab face take the
+            // write-through path (a CTA-uniform test per step)
+            bool fast = !m.g.a.sh.enabled;
+            if (!fast) {
+                constexpr int off[sizeof...(O)] = {O...};
+                constexpr int o0 = NS::sig(ARR, 0) == 0 ? off[0] : 0;
+                const long long g = (long long)m.k + o0 + m.g.a.sh.origin;
+                fast = NS::sig(ARR, 0) == 0 && g >= m.g.a.sh.lo_thr && g < m.g.a.sh.hi_thr;
+            }
+            if (fast) {
                 *(reinterpret_cast<elem_t<ARR>*>(fs.gp[ARR]) + gconst<ARR, O...>()) = v;
                 return;
             }
         }
-        m.template st<ARR, O...>(v);   // sharded launch: write-through path
+        m.template st<ARR, O...>(v);   // write-through path
     }
     template <int ARR, class... A>
     __device__ __forceinline__ void stx(A... args) const { m.template stx<ARR>(args...); }
