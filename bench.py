@@ -612,6 +612,10 @@ def per_kernel_table(peak, reps):
             row["sat_vs_orig_same_skeleton"] = ratio("accsat/naive", "original/naive")
             row["sat_vs_orig_faithful"] = round(row["original/naive"]["ms"] / row["accsat/tuned"]["ms"], 3)
             row["sat_vs_nvcc_default"] = round(row["original-nvcc/naive"]["ms"] / row["accsat/tuned"]["ms"], 3)
+            if "accsat/tb2" in row:
+                # temporal blocking vs the best single-sweep slot: same algorithmic bytes
+                # (16 B/point/sweep), about half the DRAM bytes (profiles/r02_jacobi/tb2_ncu.md)
+                row["tb2_vs_tuned"] = ratio("accsat/tb2", "accsat/tuned")
             row["bytes_per_point"] = w.bytes_per_point
         except Exception:
             pass

@@ -1,29 +1,40 @@
 // tblock.cuh — temporal blocking: two time steps of a ping-pong star stencil
 // per launch (Jacobi-7).
 //
-// A ping-pong nest (one array R read with a radius-1 star / box stencil, one
-// array W written at the point; the time loop swaps the two) advances by two
-// steps in one pass over HBM: a CTA owns a TX x TY output tile and marches
-// along k; per plane p it
-//   1. runs the nest body for step 1 on the EXTENDED tile (TX+2) x (TY+2) of
-//      plane p, reading R from a cp.async ring of planes staged with a 2-cell
-//      halo, and writes the step-1 field into a 3-plane shared-memory ring
-//      (it never reaches HBM);
-//   2. runs the same body for step 2 on the tile of plane p-1, reading the
-//      step-1 ring, and stores to W in HBM.
+// A ping-pong nest (one array R read with a radius-1 star stencil, one array
+// W written at the point; the time loop swaps the two) advances by two steps
+// in one pass over HBM.  A CTA of TX x TY threads owns a TX x TY output tile
+// and marches along k over a chunk of planes; per march plane p:
+//   0. one elected thread refills the R ring: a cp.async.bulk.tensor (TMA)
+//      box of (TX+4) x (TY+4) cells (2-cell halo) per plane into a 6-plane
+//      ring (PF = 4 planes ahead), completion on the slot's mbarrier;
+//   1. step 1 on the EXTENDED tile (TX+2) x (TY+2) of plane p: every thread
+//      its own cell, threads 0..NR-1 also one cell of the halo ring.  The
+//      cell's own column (k-1, k, k+1) lives in a register queue (one LDS of
+//      the new top plane per step), the four in-plane neighbours are LDS at
+//      compile-time offsets.  The step-1 field goes to a 3-plane shared ring
+//      — it never reaches HBM;
+//   2. (after the one barrier per plane) step 2 on the tile of plane p-1:
+//      the column again from a register queue of the thread's own step-1
+//      values, the in-plane neighbours from the step-1 ring; one STG to W.
+// The plane loop is unrolled by 6, so the ring slots, both queues and the
+// step-1 ring slot are compile-time (queue shifts are register renames).
+//
 // HBM traffic per two steps: R read once, W written once — 16 B/point for two
-// steps of an f64 nest instead of 32 (the bench reports algorithmic bytes of
-// the two steps and the DRAM bytes ncu measures, separately).  The step-1 field
-// at cells outside the iteration space (the nest's fixed boundary) is R's
-// value there: both buffers of the ping-pong must carry the same boundary
-// (true for the nest's time loop, whose boundary is never written).  The
-// same generated body as every other skeleton, so results are bit-identical
-// to two launches of the single-step kernel.
+// steps of an f64 nest instead of 32 (the bench reports the algorithmic bytes
+// of the two steps and the DRAM bytes ncu measures, separately).  The step-1
+// field outside the iteration space (the nest's fixed boundary) is R's value
+// there: both buffers of the ping-pong must carry the same boundary (true for
+// the nest's time loop, whose boundary is never written).  The same generated
+// body as every other skeleton, so results are bit-identical to two launches
+// of the single-step kernel (tests/test_gpu_parity.py).
 #pragma once
+
+#include <cstdlib>
 
 #include "../acs_device.cuh"
 #include "../registry.hpp"
-#include "stream.cuh"
+#include "../tma.cuh"
 
 namespace acs {
 
@@ -41,14 +52,13 @@ struct TbPlan {
         if (NS::NSROW != 1 || NS::srow_arr(0) != W) return false;
         for (int p = 0; p < 3; ++p)
             if (NS::srow_off(0, p) != 0) return false;
+        // a star: rows off the march plane are single centre cells (the register queue)
+        for (int r = 0; r < NS::NROW; ++r)
+            if (NS::row_off(r, 0) != 0 && (NS::row_off(r, 1) != 0 || NS::row_xlo(r) != 0 || NS::row_xhi(r) != 0))
+                return false;
         return true;
     }
 };
-
-// memory policy of one point: R from three planes (k-1, k, k+1) given as
-// 32-bit byte offsets into the kernel's shared memory (row stride RS
-// elements), the store to shared memory (step 1) or to HBM (step 2)
-extern __shared__ __align__(128) unsigned char tb_smem[];
 
 // shared-window (32-bit) loads / stores: the addresses stay plain integers, so
 // the loop-invariant parts are computed once per thread, not per access
@@ -64,24 +74,27 @@ __device__ __forceinline__ float tb_lds(unsigned a, float) {
 }
 __device__ __forceinline__ void tb_sts(unsigned a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
 __device__ __forceinline__ void tb_sts(unsigned a, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v)); }
-__device__ __forceinline__ void tb_cp_async(unsigned dst, const void* src, double) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void tb_cp_async(unsigned dst, const void* src, float) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-}
 
+// memory policy of one point: the column (k-1, k, k+1) from registers, the
+// in-plane neighbours from shared memory at `a` (this cell's byte address in
+// the current plane, row stride RS elements); the store lands in *out
 template <class T, int RS>
 struct TbMem {
-    unsigned o[3];
-    T* out;        // the point's value (a register after inlining): stores are predicated by the caller
+    unsigned a;
+    T qm, q0, qp;
+    T* out;
     template <int ARR>
     using elem_t = T;
     template <int ARR, int... O>
     __device__ __forceinline__ T ld() const {
         constexpr int off[sizeof...(O)] = {O...};
-        constexpr int c = (off[1] * RS + off[2]) * (int)sizeof(T);
-        return tb_lds(o[off[0] + 1] + (unsigned)c, T(0));
+        if constexpr (off[1] == 0 && off[2] == 0) {
+            return off[0] < 0 ? qm : (off[0] > 0 ? qp : q0);
+        } else {
+            static_assert(off[0] == 0, "tb2: off-plane loads are centre cells (a star stencil)");
+            constexpr int c = (off[1] * RS + off[2]) * (int)sizeof(T);
+            return tb_lds(a + (unsigned)c, T(0));
+        }
     }
     template <int ARR, int... O>
     __device__ __forceinline__ void st(T v) const {
@@ -95,136 +108,190 @@ struct TbMem {
     __device__ __forceinline__ void stx(A...) const {}
 };
 
-template <class NS, class T, int FORM, int TX, int TY, int BX, int BY, int PF>
-__global__ void __launch_bounds__(BX* BY) tb2_kernel(const __grid_constant__ KernelArgs<NS> args, int kchunk) {
-    using TP = TbPlan<NS>;
-    constexpr int R = TP::R, W = TP::W;
-    constexpr int EX = TX + 4, EY = TY + 4;   // staged R plane (2-cell halo)
-    constexpr int IX = TX + 2, IY = TY + 2;   // step-1 plane (extended tile)
-    constexpr int D = 3 + PF;                 // R ring planes
-    constexpr int NT = BX * BY;
-    // every thread owns fixed cells of each per-plane job (no index math per plane)
-    constexpr int N0 = (EY * EX + NT - 1) / NT;   // staged cells
-    constexpr int N1 = (IY * IX + NT - 1) / NT;   // step-1 points
-    constexpr int N2 = (TY * TX + NT - 1) / NT;   // step-2 points
-    const unsigned sbase = (unsigned)__cvta_generic_to_shared(tb_smem);
-    constexpr unsigned PLANE = EY * EX * sizeof(T), IPLANE = IY * IX * sizeof(T);
-    const unsigned IBASE = sbase + D * PLANE;
-    const int tid = threadIdx.y * BX + threadIdx.x;
+template <int TX, int TY, int PF, class T>
+struct TbGeom {
+    static constexpr int EX = TX + 4, EY = TY + 4;     // staged R box (2-cell halo)
+    static constexpr int IX = TX + 2, IY = TY + 2;     // step-1 plane (extended tile)
+    static constexpr int D = 6;                        // R ring planes (PF = 4 in flight)
+    static constexpr int NT = TX * TY;
+    static constexpr int NR = IX * IY - TX * TY;       // halo-ring cells of the extended tile
+    static constexpr unsigned PLANE = ((EY * EX * (int)sizeof(T) + 127) / 128) * 128;
+    static constexpr unsigned IPLANE = ((IY * IX * (int)sizeof(T) + 127) / 128) * 128;
+    static constexpr int smem = D * PLANE + 3 * IPLANE + D * 8;
+    static_assert(PF == D - 2, "tb2: the ring is 6 planes deep (PF = 4)");
+    static_assert(NR <= NT, "tb2: the halo ring needs at most one cell per thread");
+    static_assert((EX * (int)sizeof(T)) % 16 == 0, "tb2: TMA box rows are 16-byte multiples");
+};
+
+template <class NS, class T, int FORM, int TX, int TY, int PF>
+__global__ void __launch_bounds__(TX* TY, 3) tb2_kernel(const __grid_constant__ KernelArgs<NS> args,
+                                                     const __grid_constant__ CUtensorMap rmap, int adjx, int kchunk) {
+    using G = TbGeom<TX, TY, PF, T>;
+    constexpr int R = TbPlan<NS>::R, W = TbPlan<NS>::W;
+    constexpr int EX = G::EX, IX = G::IX, IY = G::IY, D = G::D, NR = G::NR;
+    constexpr unsigned PLANE = G::PLANE, IPLANE = G::IPLANE, ES = sizeof(T);
+    extern __shared__ __align__(128) unsigned char tb_smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tb_smem + D * PLANE + 3 * IPLANE);
+    const unsigned rbase = smem_u32(tb_smem), ibase = rbase + D * PLANE;
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
     const int lo0 = args.lo[0], hi0 = args.hi[0], lo1 = args.lo[1], hi1 = args.hi[1], lo2 = args.lo[2],
               hi2 = args.hi[2];
     const int orgx = lo2 + blockIdx.x * TX, orgy = lo1 + blockIdx.y * TY;
     const int kb = lo0 + blockIdx.z * kchunk, ke = min(kb + kchunk, hi0);
-    const T* rb = reinterpret_cast<const T*>(args.arr[R].base);
-    T* wb = reinterpret_cast<T*>(args.arr[W].base);
-    const long long r0 = args.arr[R].stride[0], w0 = args.arr[W].stride[0];
-    const int abase = kb - 2;                 // R planes abase .. ke + 1
+    const int abase = kb - 2;                 // R planes abase .. ke + 1 (TMA zero-fills outside the array)
     const int alast = ke + 1;
 
-    // staged cells: valid (inside the cells a step reads) -> element offset in the plane
-    unsigned soff[N0];
-    bool sv[N0];
-#pragma unroll
-    for (int i = 0; i < N0; ++i) {
-        const int e = tid + i * NT, by = e / EX, bx = e - by * EX;
-        const int y = orgy - 2 + by, x = orgx - 2 + bx;
-        sv[i] = e < EY * EX && y >= lo1 - 1 && y <= hi1 && x >= lo2 - 1 && x <= hi2;
-        soff[i] = sv[i] ? (unsigned)((long long)y * args.arr[R].stride[1] + (long long)x * args.arr[R].stride[2]) : 0u;
-    }
-    // step-1 points: 1 = run the body, 2 = copy R (fixed boundary), 0 = nothing
-    int s1[N1], b1[N1], y1[N1], x1[N1];
-#pragma unroll
-    for (int i = 0; i < N1; ++i) {
-        const int e = tid + i * NT, ey = e / IX, ex = e - ey * IX;
-        y1[i] = orgy - 1 + ey;
-        x1[i] = orgx - 1 + ex;
-        b1[i] = e < IY * IX ? (ey + 1) * EX + ex + 1 : EX + 1;   // spare lanes read a safe in-box cell
-        const bool in = y1[i] >= lo1 && y1[i] < hi1 && x1[i] >= lo2 && x1[i] < hi2;
-        const bool band = y1[i] >= lo1 - 1 && y1[i] <= hi1 && x1[i] >= lo2 - 1 && x1[i] <= hi2;
-        s1[i] = e >= IY * IX ? 0 : (in ? 1 : (band ? 2 : 0));
-    }
-    // step-2 points: in the domain -> step-1 ring index and global offset of W
-    bool v2[N2];
-    int i2[N2], y2[N2], x2[N2];
-    long long g2[N2];
-#pragma unroll
-    for (int i = 0; i < N2; ++i) {
-        const int o = tid + i * NT, oy = o / TX, ox = o - oy * TX;
-        y2[i] = orgy + oy;
-        x2[i] = orgx + ox;
-        v2[i] = o < TY * TX && y2[i] < hi1 && x2[i] < hi2;
-        i2[i] = o < TY * TX ? (oy + 1) * IX + ox + 1 : IX + 1;
-        g2[i] = (long long)y2[i] * args.arr[W].stride[1] + (long long)x2[i] * args.arr[W].stride[2];
-    }
+    // own cell: box / step-1-plane byte offsets, domain flags, W offset
+    const int x = orgx + tx, y = orgy + ty;
+    const unsigned obox = (unsigned)((ty + 2) * EX + tx + 2) * ES;
+    const unsigned oint = (unsigned)((ty + 1) * IX + tx + 1) * ES;
+    const bool own_in = x < hi2 && y < hi1;
+    T* wp = reinterpret_cast<T*>(args.arr[W].base) + (long long)y * args.arr[W].stride[1] +
+            (long long)x * args.arr[W].stride[2];
+    const long long w0 = args.arr[W].stride[0];
+    // halo-ring cell (threads 0..NR-1): top row, bottom row, left column, right column
+    int rex = 0, rey = 0;
+    if (tid < IX) {
+        rex = tid;
+        rey = 0;
+    } else if (tid < 2 * IX) {
+        rex = tid - IX;
+        rey = IY - 1;
+    } else if (tid < 2 * IX + TY) {
+        rex = 0;
+        rey = tid - 2 * IX + 1;
+    } else if (tid < NR) {
+        rex = IX - 1;
+        rey = tid - 2 * IX - TY + 1;
+    }                                         // other threads: cell (0, 0), in the box (never stored)
+    const bool has_ring = tid < NR;
+    const int rx = orgx - 1 + rex, ry = orgy - 1 + rey;
+    const bool ring_in = rx >= lo2 && rx < hi2 && ry >= lo1 && ry < hi1;
+    const unsigned rbox = (unsigned)((rey + 1) * EX + rex + 1) * ES;
+    const unsigned rint = (unsigned)(rey * IX + rex) * ES;
 
-    auto issue = [&](int a) {                 // cp.async of R plane a, one commit group
-        if (a <= alast && a >= lo0 - 1 && a <= hi0) {
-            const unsigned dst = sbase + ((a - abase) % D) * PLANE + tid * (unsigned)sizeof(T);
-            const T* src = rb + (long long)a * r0;
-#pragma unroll
-            for (int i = 0; i < N0; ++i)
-                if (sv[i]) tb_cp_async(dst + i * NT * (unsigned)sizeof(T), src + soff[i], T(0));
-        }
-        cp_async_commit();
+    // R plane a lives in ring slot (a - abase) % D, its fill number (a - abase) / D
+    auto issue = [&](int a, int s) {          // TMA of R plane a into slot s (elected thread)
+        fence_proxy_async();
+        mbar_expect_tx(&bars[s], (uint32_t)(G::EY * EX * ES));
+        const int c[3] = {orgx - 2 + adjx, orgy - 2, a};
+        tma_load<3>(tb_smem + s * PLANE, &rmap, c, &bars[s]);
     };
-    for (int i = 0; i < D - 1; ++i) issue(abase + i);
+
+    if (tid == 0) {
+        tma_prefetch_desc(&rmap);
+        for (int s = 0; s < D; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int s = 0; s < D && abase + s <= alast; ++s) issue(abase + s, s);
+
+    // register queues: R column of the own / ring cell, step-1 column of the own cell
+    T rq[3], gq[3], sq[3];
+    mbar_wait(&bars[0], 0);
+    mbar_wait(&bars[1], 0);
+    rq[0] = tb_lds(rbase + obox, T(0));
+    rq[1] = tb_lds(rbase + PLANE + obox, T(0));
+    gq[0] = tb_lds(rbase + rbox, T(0));
+    gq[1] = tb_lds(rbase + PLANE + rbox, T(0));
+    rq[2] = gq[2] = sq[0] = sq[1] = sq[2] = T(0);
+    __syncthreads();                          // plane abase's slot is free for the refill
 
     int pt[3];
-    int slot = (kb - 1 - abase) % D;          // ring slot of plane p
-    for (int p = kb - 1; p <= ke; ++p) {
-        issue(p + D - 2);                     // plane p+1+PF into the slot plane p-2 used
-        cp_async_wait<PF>();                  // plane p+1 has landed (this thread's copies)
-        __syncthreads();
-        // 1. step 1 on the extended tile of plane p -> step-1 ring
-        {
-            const unsigned a1 = sbase + slot * PLANE;
-            const unsigned a0 = sbase + (slot == 0 ? D - 1 : slot - 1) * PLANE;
-            const unsigned a2 = sbase + (slot == D - 1 ? 0 : slot + 1) * PLANE;
-            const unsigned ip = IBASE + (p % 3) * IPLANE;
+    // the plane loop, unrolled by D = 6: plane p = p0 + u has R slot (u + 1) % 6,
+    // step-1 slot u % 3 and queue positions u % 3 .. (u + 2) % 3 — all compile-time
+    uint32_t fill = 0;                        // (p0 - kb + 1) / 6: fill number of slot 1.. at phase 0
+    for (int p0 = kb - 1; p0 <= ke; p0 += D, ++fill) {
+#pragma unroll
+        for (int u = 0; u < D; ++u) {
+            const int p = p0 + u;
+            if (p > ke) break;
+            // queue slots of this phase: plane p-1, p, p+1 = (u), (u+1), (u+2) mod 3 (R queues);
+            // step-1 values of planes p-2, p-1, p likewise (sq)
+            const int qm = u % 3, qc = (u + 1) % 3, qn = (u + 2) % 3;
+            const int sl_p = (u + 1) % D, sl_n = (u + 2) % D, sl_free = u % D;
+            // slot u held plane p - 1 (read by the previous phase, before its barrier)
+            if (tid == 0 && p - 1 + D <= alast) issue(p - 1 + D, sl_free);
+            mbar_wait(&bars[sl_n], (fill + (u + 2) / D) & 1u);
+            const unsigned sp = rbase + sl_p * PLANE, sn = rbase + sl_n * PLANE;
+            const unsigned ip = ibase + (unsigned)(u % 3) * IPLANE;    // step-1 slot of plane p
             const bool pin = p >= lo0 && p < hi0;
-            const bool pvalid = p >= lo0 - 1 && p <= hi0;
-            // every point runs the body on in-box values (branch-free, the loads
-            // of all points in flight together); the store is predicated
-#pragma unroll
-            for (int i = 0; i < N1; ++i) {
-                const unsigned bo = (unsigned)b1[i] * sizeof(T), so = ip + (tid + i * NT) * (unsigned)sizeof(T);
+            // 1. step 1 on plane p: own cell, then the ring cell
+            {
+                rq[qn] = tb_lds(sn + obox, T(0));
+                T v = T(0);
+                TbMem<T, EX> m{sp + obox, rq[qm], rq[qc], rq[qn], &v};
                 pt[0] = p;
-                pt[1] = y1[i];
-                pt[2] = x1[i];
-                T v = T(0);
-                TbMem<T, EX> m{{a0 + bo, a1 + bo, a2 + bo}, &v};
+                pt[1] = y;
+                pt[2] = x;
                 NS::template body<FORM>(m, args.s, pt);
-                const T c = tb_lds(a1 + bo, T(0));    // fixed boundary: the field keeps R's value
-                if (pvalid && s1[i] != 0) tb_sts(so, pin && s1[i] == 1 ? v : c);
+                const T s1 = pin && own_in ? v : rq[qc];
+                sq[qn] = s1;
+                tb_sts(ip + oint, s1);
             }
-        }
-        __syncthreads();
-        // 2. step 2 on the tile of plane q = p - 1 -> W in HBM
-        const int q = p - 1;
-        if (q >= kb && q < ke) {
-            const unsigned i0 = IBASE + ((q + 2) % 3) * IPLANE;
-            const unsigned i1 = IBASE + (q % 3) * IPLANE;
-            const unsigned ii2 = IBASE + ((q + 1) % 3) * IPLANE;
-            T* wq = wb + (long long)q * w0;
-#pragma unroll
-            for (int i = 0; i < N2; ++i) {
-                const unsigned bo = (unsigned)i2[i] * sizeof(T);
+            if (has_ring) {
+                gq[qn] = tb_lds(sn + rbox, T(0));
+                T v = T(0);
+                TbMem<T, EX> m{sp + rbox, gq[qm], gq[qc], gq[qn], &v};
+                pt[0] = p;
+                pt[1] = ry;
+                pt[2] = rx;
+                NS::template body<FORM>(m, args.s, pt);
+                tb_sts(ip + rint, pin && ring_in ? v : gq[qc]);
+            }
+            __syncthreads();
+            // 2. step 2 on plane q = p - 1 (its step-1 slot is u - 1 mod 3)
+            const int q = p - 1;
+            if (q >= kb) {
+                const unsigned iq = ibase + (unsigned)((u + 2) % 3) * IPLANE;   // plane p - 1
+                T v = T(0);
+                // the own step-1 column of planes q-1, q, q+1 = p-2, p-1, p
+                TbMem<T, IX> m{iq + oint, sq[qm], sq[qc], sq[qn], &v};
                 pt[0] = q;
-                pt[1] = y2[i];
-                pt[2] = x2[i];
-                T v = T(0);
-                TbMem<T, IX> m{{i0 + bo, i1 + bo, ii2 + bo}, &v};
+                pt[1] = y;
+                pt[2] = x;
                 NS::template body<FORM>(m, args.s, pt);
-                if (v2[i]) wq[g2[i]] = v;
+                if (own_in) wp[(long long)q * w0] = v;
             }
         }
-        slot = slot == D - 1 ? 0 : slot + 1;
     }
 }
 
-template <class NS, class T, int FORM, int TX, int TY, int BX, int BY, int PF>
+template <class NS, class T, int TX, int TY, int PF>
+bool encode_tb_map(const LaunchReq& r, CUtensorMap& map, int& adjx) {
+    constexpr int R = TbPlan<NS>::R;
+    using G = TbGeom<TX, TY, PF, T>;
+    EncodeTiledFn enc = tma_encoder();
+    if (!enc) return false;
+    const acs_array* d = nullptr;
+    for (int i = 0; i < r.n_arrays; ++i)
+        if (std::strcmp(r.arrays[i].name, NS::array_names[R]) == 0) d = &r.arrays[i];
+    if (!d || d->ndim != 3) return false;
+    long long st[3];
+    bool rm = true;
+    for (int p = 0; p < 3; ++p) rm = rm && d->strides[p] == 0;
+    st[2] = rm ? 1 : d->strides[2];
+    st[1] = rm ? d->dims[2] : d->strides[1];
+    st[0] = rm ? d->dims[1] * d->dims[2] : d->strides[0];
+    const int es = (int)sizeof(T);
+    const int mis = (int)(reinterpret_cast<uintptr_t>(d->data) % 16);
+    if (st[2] != 1 || mis % es != 0 || (st[1] * es) % 16 != 0 || (st[0] * es) % 16 != 0 || st[0] < st[1]) return false;
+    adjx = mis / es;
+    cuuint64_t gdim[3] = {(cuuint64_t)(d->dims[2] + adjx), (cuuint64_t)d->dims[1], (cuuint64_t)d->dims[0]};
+    cuuint64_t gstr[2] = {(cuuint64_t)(st[1] * es), (cuuint64_t)(st[0] * es)};
+    cuuint32_t box[3] = {(cuuint32_t)G::EX, (cuuint32_t)G::EY, 1u};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    void* base = static_cast<char*>(d->data) - (size_t)adjx * es;
+    const CUtensorMapDataType dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    return enc(&map, dt, 3u, base, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class NS, class T, int FORM, int TX, int TY, int PF>
 acs_status launch_tb2(const LaunchReq& r) {
     static_assert(TbPlan<NS>::usable(), "tb2: not a ping-pong star stencil");
+    using G = TbGeom<TX, TY, PF, T>;
     KernelArgs<NS> ka;
     bool empty = false;
     acs_status st = bind<NS, std::is_same<T, float>::value>(r, ka, empty);
@@ -233,32 +300,43 @@ acs_status launch_tb2(const LaunchReq& r) {
         set_error("tb2: two-step launches are not sharded");
         return ACS_E_ARG;
     }
-    constexpr int smem = ((3 + PF) * (TY + 4) * (TX + 4) + 3 * (TY + 2) * (TX + 2)) * (int)sizeof(T);
-    auto kern = tb2_kernel<NS, T, FORM, TX, TY, BX, BY, PF>;
+    auto kern = tb2_kernel<NS, T, FORM, TX, TY, PF>;
     if (r.preload) return preload_fn((const void*)kern);
+    CUtensorMap map;
+    int adjx = 0;
+    if (!encode_tb_map<NS, T, TX, TY, PF>(r, map, adjx)) {
+        set_error(std::string("tb2 (") + NS::array_names[TbPlan<NS>::R] +
+                  "): the TMA cannot describe this layout (16-byte aligned pitches needed); use native strides");
+        return ACS_E_LAYOUT;
+    }
     static std::atomic<unsigned long long> attr_done{0};
-    set_smem_attr_once(kern, smem, attr_done);
+    set_smem_attr_once(kern, G::smem, attr_done);
     const long long nx = ka.hi[2] - ka.lo[2], ny = ka.hi[1] - ka.lo[1], nz = ka.hi[0] - ka.lo[0];
     const long long tiles = ((nx + TX - 1) / TX) * ((ny + TY - 1) / TY);
-    // enough CTAs for ~4 resident per SM; chunks long enough to amortise the 2 extra planes
-    long long kchunk = (nz * tiles + 148LL * 4 - 1) / (148LL * 4);
-    if (kchunk < 16) kchunk = 16;
+    // ~4 waves of 2 resident CTAs per SM; chunks long enough to amortise the 3 extra planes
+    long long kchunk = (nz * tiles + 148LL * 8 - 1) / (148LL * 8);
+    static const long long kch_env = [] {   // experiment knob (tools/gpu), not a tuning path
+        const char* e = std::getenv("ACS_TB_KCHUNK");
+        return e ? std::atoll(e) : 0LL;
+    }();
+    if (kch_env > 0) kchunk = kch_env;
+    if (kchunk < 12) kchunk = 12;
     if (kchunk > nz) kchunk = nz;
     const long long chunks = (nz + kchunk - 1) / kchunk;
     dim3 grid((unsigned)((nx + TX - 1) / TX), (unsigned)((ny + TY - 1) / TY), (unsigned)chunks);
-    kern<<<grid, dim3(BX, BY, 1), smem, r.stream>>>(ka, (int)kchunk);
+    kern<<<grid, dim3(TX, TY, 1), G::smem, r.stream>>>(ka, map, adjx, (int)kchunk);
     return check_launch("tb2");
 }
 
-template <class NS, class T, int TX, int TY, int BX, int BY, int PF>
+template <class NS, class T, int TX, int TY, int PF>
 void fill_tb2(Entry& e, int prec) {
-    e.tb2[prec][0] = &launch_tb2<NS, T, 0, TX, TY, BX, BY, PF>;
-    e.tb2[prec][1] = &launch_tb2<NS, T, 1, TX, TY, BX, BY, PF>;
-    e.tb2[prec][2] = &launch_tb2<NS, T, 2, TX, TY, BX, BY, PF>;
-    e.tb2[prec][3] = &launch_tb2<NS, T, 3, TX, TY, BX, BY, PF>;
-    e.tb2[prec][4] = &launch_tb2<NS, T, 4, TX, TY, BX, BY, PF>;
-    e.tb2_name[prec] = "temporal block x2, tile " + std::to_string(TX) + "x" + std::to_string(TY) + " block " +
-                       std::to_string(BX) + "x" + std::to_string(BY) + " pf " + std::to_string(PF);
+    e.tb2[prec][0] = &launch_tb2<NS, T, 0, TX, TY, PF>;
+    e.tb2[prec][1] = &launch_tb2<NS, T, 1, TX, TY, PF>;
+    e.tb2[prec][2] = &launch_tb2<NS, T, 2, TX, TY, PF>;
+    e.tb2[prec][3] = &launch_tb2<NS, T, 3, TX, TY, PF>;
+    e.tb2[prec][4] = &launch_tb2<NS, T, 4, TX, TY, PF>;
+    e.tb2_name[prec] = "temporal block x2 (TMA ring, register columns), tile " + std::to_string(TX) + "x" +
+                       std::to_string(TY) + " pf " + std::to_string(PF);
     e.tb2_read = TbPlan<NS>::R;
 }
 

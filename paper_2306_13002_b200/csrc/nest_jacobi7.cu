@@ -21,7 +21,7 @@ void register_jacobi7() {
         fill_march<gen::jacobi7, double, 0, 128, 16, 128, 4, 2>(e, 0);
         fill_march<gen::jacobi7, double, 0, 128, 4, 128, 2, 3>(e, 0);
         fill_march<gen::jacobi7, double, 0, 128, 16, 64, 4, 2, 2>(e, 0);
-        fill_tb2<gen::jacobi7, double, 64, 8, 64, 4, 2>(e, 0);   // two sweeps per launch
+        fill_tb2<gen::jacobi7, double, 32, 16, 4>(e, 0);   // two sweeps per launch
         register_entry(&e);
     }
 }
