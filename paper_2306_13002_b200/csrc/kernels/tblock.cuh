@@ -76,12 +76,15 @@ __device__ __forceinline__ void tb_sts(unsigned a, double v) { asm volatile("st.
 __device__ __forceinline__ void tb_sts(unsigned a, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v)); }
 
 // memory policy of one point: the column (k-1, k, k+1) from registers, the
+// y neighbours from registers when the thread owns them too, the other
 // in-plane neighbours from shared memory at `a` (this cell's byte address in
 // the current plane, row stride RS elements); the store lands in *out
 template <class T, int RS>
 struct TbMem {
     unsigned a;
     T qm, q0, qp;
+    T ym, yp;      // in-plane y-1 / y+1 neighbours held by this thread (its other cells), if hym / hyp
+    bool hym, hyp; // compile-time constants once the cell loop is unrolled
     T* out;
     template <int ARR>
     using elem_t = T;
@@ -92,6 +95,10 @@ struct TbMem {
             return off[0] < 0 ? qm : (off[0] > 0 ? qp : q0);
         } else {
             static_assert(off[0] == 0, "tb2: off-plane loads are centre cells (a star stencil)");
+            if constexpr (off[1] == -1 && off[2] == 0)
+                if (hym) return ym;
+            if constexpr (off[1] == 1 && off[2] == 0)
+                if (hyp) return yp;
             constexpr int c = (off[1] * RS + off[2]) * (int)sizeof(T);
             return tb_lds(a + (unsigned)c, T(0));
         }
@@ -108,25 +115,27 @@ struct TbMem {
     __device__ __forceinline__ void stx(A...) const {}
 };
 
-template <int TX, int TY, int PF, class T>
+template <int TX, int TY, int NY, int PF, class T>
 struct TbGeom {
     static constexpr int EX = TX + 4, EY = TY + 4;     // staged R box (2-cell halo)
     static constexpr int IX = TX + 2, IY = TY + 2;     // step-1 plane (extended tile)
     static constexpr int D = 6;                        // R ring planes (PF = 4 in flight)
-    static constexpr int NT = TX * TY;
+    static constexpr int NT = TX * TY / NY;           // threads: NY cells of a column each
     static constexpr int NR = IX * IY - TX * TY;       // halo-ring cells of the extended tile
     static constexpr unsigned PLANE = ((EY * EX * (int)sizeof(T) + 127) / 128) * 128;
     static constexpr unsigned IPLANE = ((IY * IX * (int)sizeof(T) + 127) / 128) * 128;
     static constexpr int smem = D * PLANE + 3 * IPLANE + D * 8;
     static_assert(PF == D - 2, "tb2: the ring is 6 planes deep (PF = 4)");
     static_assert(NR <= NT, "tb2: the halo ring needs at most one cell per thread");
+    static_assert(TY % NY == 0, "tb2: NY divides the tile height");
     static_assert((EX * (int)sizeof(T)) % 16 == 0, "tb2: TMA box rows are 16-byte multiples");
 };
 
-template <class NS, class T, int FORM, int TX, int TY, int PF>
-__global__ void __launch_bounds__(TX* TY, 3) tb2_kernel(const __grid_constant__ KernelArgs<NS> args,
-                                                     const __grid_constant__ CUtensorMap rmap, int adjx, int kchunk) {
-    using G = TbGeom<TX, TY, PF, T>;
+template <class NS, class T, int FORM, int TX, int TY, int NY, int PF, int MINB>
+__global__ void __launch_bounds__(TX* TY / NY, MINB) tb2_kernel(const __grid_constant__ KernelArgs<NS> args,
+                                                             const __grid_constant__ CUtensorMap rmap, int adjx,
+                                                             int kchunk) {
+    using G = TbGeom<TX, TY, NY, PF, T>;
     constexpr int R = TbPlan<NS>::R, W = TbPlan<NS>::W;
     constexpr int EX = G::EX, IX = G::IX, IY = G::IY, D = G::D, NR = G::NR;
     constexpr unsigned PLANE = G::PLANE, IPLANE = G::IPLANE, ES = sizeof(T);
@@ -141,15 +150,18 @@ __global__ void __launch_bounds__(TX* TY, 3) tb2_kernel(const __grid_constant__ 
     const int abase = kb - 2;                 // R planes abase .. ke + 1 (TMA zero-fills outside the array)
     const int alast = ke + 1;
 
-    // own cell: box / step-1-plane byte offsets, domain flags, W offset
-    const int x = orgx + tx, y = orgy + ty;
-    const unsigned obox = (unsigned)((ty + 2) * EX + tx + 2) * ES;
-    const unsigned oint = (unsigned)((ty + 1) * IX + tx + 1) * ES;
-    const bool own_in = x < hi2 && y < hi1;
+    // own cells (x, y + c), c < NY: box / step-1-plane byte offsets of cell 0, domain flags, W offset
+    const int x = orgx + tx, y = orgy + ty * NY;
+    const unsigned obox = (unsigned)((ty * NY + 2) * EX + tx + 2) * ES;
+    const unsigned oint = (unsigned)((ty * NY + 1) * IX + tx + 1) * ES;
+    bool own_in[NY];
+#pragma unroll
+    for (int c = 0; c < NY; ++c) own_in[c] = x < hi2 && y + c < hi1;
     T* wp = reinterpret_cast<T*>(args.arr[W].base) + (long long)y * args.arr[W].stride[1] +
             (long long)x * args.arr[W].stride[2];
-    const long long w0 = args.arr[W].stride[0];
-    // halo-ring cell (threads 0..NR-1): top row, bottom row, left column, right column
+    const long long w0 = args.arr[W].stride[0], w1 = args.arr[W].stride[1];
+    // halo-ring cell (threads 0..NR-1): top row, bottom row, then the left and right columns
+    // interleaved (lane pairs share a row: half the bank conflicts of a column walk)
     int rex = 0, rey = 0;
     if (tid < IX) {
         rex = tid;
@@ -157,12 +169,9 @@ __global__ void __launch_bounds__(TX* TY, 3) tb2_kernel(const __grid_constant__ 
     } else if (tid < 2 * IX) {
         rex = tid - IX;
         rey = IY - 1;
-    } else if (tid < 2 * IX + TY) {
-        rex = 0;
-        rey = tid - 2 * IX + 1;
     } else if (tid < NR) {
-        rex = IX - 1;
-        rey = tid - 2 * IX - TY + 1;
+        rex = ((tid - 2 * IX) & 1) ? IX - 1 : 0;
+        rey = ((tid - 2 * IX) >> 1) + 1;
     }                                         // other threads: cell (0, 0), in the box (never stored)
     const bool has_ring = tid < NR;
     const int rx = orgx - 1 + rex, ry = orgy - 1 + rey;
@@ -187,15 +196,19 @@ __global__ void __launch_bounds__(TX* TY, 3) tb2_kernel(const __grid_constant__ 
     if (tid == 0)
         for (int s = 0; s < D && abase + s <= alast; ++s) issue(abase + s, s);
 
-    // register queues: R column of the own / ring cell, step-1 column of the own cell
-    T rq[3], gq[3], sq[3];
+    // register queues: R column of the own / ring cells, step-1 column of the own cells
+    T rq[NY][3], gq[3], sq[NY][3];
     mbar_wait(&bars[0], 0);
     mbar_wait(&bars[1], 0);
-    rq[0] = tb_lds(rbase + obox, T(0));
-    rq[1] = tb_lds(rbase + PLANE + obox, T(0));
+#pragma unroll
+    for (int c = 0; c < NY; ++c) {
+        rq[c][0] = tb_lds(rbase + obox + c * EX * ES, T(0));
+        rq[c][1] = tb_lds(rbase + PLANE + obox + c * EX * ES, T(0));
+        rq[c][2] = sq[c][0] = sq[c][1] = sq[c][2] = T(0);
+    }
     gq[0] = tb_lds(rbase + rbox, T(0));
     gq[1] = tb_lds(rbase + PLANE + rbox, T(0));
-    rq[2] = gq[2] = sq[0] = sq[1] = sq[2] = T(0);
+    gq[2] = T(0);
     __syncthreads();                          // plane abase's slot is free for the refill
 
     int pt[3];
@@ -217,23 +230,26 @@ __global__ void __launch_bounds__(TX* TY, 3) tb2_kernel(const __grid_constant__ 
             const unsigned sp = rbase + sl_p * PLANE, sn = rbase + sl_n * PLANE;
             const unsigned ip = ibase + (unsigned)(u % 3) * IPLANE;    // step-1 slot of plane p
             const bool pin = p >= lo0 && p < hi0;
-            // 1. step 1 on plane p: own cell, then the ring cell
-            {
-                rq[qn] = tb_lds(sn + obox, T(0));
+            // 1. step 1 on plane p: own cells, then the ring cell
+#pragma unroll
+            for (int c = 0; c < NY; ++c) rq[c][qn] = tb_lds(sn + obox + c * EX * ES, T(0));
+#pragma unroll
+            for (int c = 0; c < NY; ++c) {
                 T v = T(0);
-                TbMem<T, EX> m{sp + obox, rq[qm], rq[qc], rq[qn], &v};
+                TbMem<T, EX> m{sp + obox + c * EX * ES, rq[c][qm], rq[c][qc], rq[c][qn], rq[c > 0 ? c - 1 : 0][qc],
+                               rq[c < NY - 1 ? c + 1 : 0][qc], c > 0, c < NY - 1, &v};
                 pt[0] = p;
-                pt[1] = y;
+                pt[1] = y + c;
                 pt[2] = x;
                 NS::template body<FORM>(m, args.s, pt);
-                const T s1 = pin && own_in ? v : rq[qc];
-                sq[qn] = s1;
-                tb_sts(ip + oint, s1);
+                const T s1 = pin && own_in[c] ? v : rq[c][qc];
+                sq[c][qn] = s1;
+                tb_sts(ip + oint + c * IX * ES, s1);
             }
             if (has_ring) {
                 gq[qn] = tb_lds(sn + rbox, T(0));
                 T v = T(0);
-                TbMem<T, EX> m{sp + rbox, gq[qm], gq[qc], gq[qn], &v};
+                TbMem<T, EX> m{sp + rbox, gq[qm], gq[qc], gq[qn], T(0), T(0), false, false, &v};
                 pt[0] = p;
                 pt[1] = ry;
                 pt[2] = rx;
@@ -245,23 +261,27 @@ __global__ void __launch_bounds__(TX* TY, 3) tb2_kernel(const __grid_constant__ 
             const int q = p - 1;
             if (q >= kb) {
                 const unsigned iq = ibase + (unsigned)((u + 2) % 3) * IPLANE;   // plane p - 1
-                T v = T(0);
-                // the own step-1 column of planes q-1, q, q+1 = p-2, p-1, p
-                TbMem<T, IX> m{iq + oint, sq[qm], sq[qc], sq[qn], &v};
-                pt[0] = q;
-                pt[1] = y;
-                pt[2] = x;
-                NS::template body<FORM>(m, args.s, pt);
-                if (own_in) wp[(long long)q * w0] = v;
+#pragma unroll
+                for (int c = 0; c < NY; ++c) {
+                    T v = T(0);
+                    // the own step-1 column of planes q-1, q, q+1 = p-2, p-1, p
+                    TbMem<T, IX> m{iq + oint + c * IX * ES, sq[c][qm], sq[c][qc], sq[c][qn], sq[c > 0 ? c - 1 : 0][qc],
+                                   sq[c < NY - 1 ? c + 1 : 0][qc], c > 0, c < NY - 1, &v};
+                    pt[0] = q;
+                    pt[1] = y + c;
+                    pt[2] = x;
+                    NS::template body<FORM>(m, args.s, pt);
+                    if (own_in[c]) wp[(long long)q * w0 + c * w1] = v;
+                }
             }
         }
     }
 }
 
-template <class NS, class T, int TX, int TY, int PF>
+template <class NS, class T, int TX, int TY, int NY, int PF>
 bool encode_tb_map(const LaunchReq& r, CUtensorMap& map, int& adjx) {
     constexpr int R = TbPlan<NS>::R;
-    using G = TbGeom<TX, TY, PF, T>;
+    using G = TbGeom<TX, TY, NY, PF, T>;
     EncodeTiledFn enc = tma_encoder();
     if (!enc) return false;
     const acs_array* d = nullptr;
@@ -288,10 +308,10 @@ bool encode_tb_map(const LaunchReq& r, CUtensorMap& map, int& adjx) {
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <class NS, class T, int FORM, int TX, int TY, int PF>
+template <class NS, class T, int FORM, int TX, int TY, int NY, int PF, int MINB>
 acs_status launch_tb2(const LaunchReq& r) {
     static_assert(TbPlan<NS>::usable(), "tb2: not a ping-pong star stencil");
-    using G = TbGeom<TX, TY, PF, T>;
+    using G = TbGeom<TX, TY, NY, PF, T>;
     KernelArgs<NS> ka;
     bool empty = false;
     acs_status st = bind<NS, std::is_same<T, float>::value>(r, ka, empty);
@@ -300,11 +320,11 @@ acs_status launch_tb2(const LaunchReq& r) {
         set_error("tb2: two-step launches are not sharded");
         return ACS_E_ARG;
     }
-    auto kern = tb2_kernel<NS, T, FORM, TX, TY, PF>;
+    auto kern = tb2_kernel<NS, T, FORM, TX, TY, NY, PF, MINB>;
     if (r.preload) return preload_fn((const void*)kern);
     CUtensorMap map;
     int adjx = 0;
-    if (!encode_tb_map<NS, T, TX, TY, PF>(r, map, adjx)) {
+    if (!encode_tb_map<NS, T, TX, TY, NY, PF>(r, map, adjx)) {
         set_error(std::string("tb2 (") + NS::array_names[TbPlan<NS>::R] +
                   "): the TMA cannot describe this layout (16-byte aligned pitches needed); use native strides");
         return ACS_E_LAYOUT;
@@ -313,8 +333,8 @@ acs_status launch_tb2(const LaunchReq& r) {
     set_smem_attr_once(kern, G::smem, attr_done);
     const long long nx = ka.hi[2] - ka.lo[2], ny = ka.hi[1] - ka.lo[1], nz = ka.hi[0] - ka.lo[0];
     const long long tiles = ((nx + TX - 1) / TX) * ((ny + TY - 1) / TY);
-    // ~4 waves of 2 resident CTAs per SM; chunks long enough to amortise the 3 extra planes
-    long long kchunk = (nz * tiles + 148LL * 8 - 1) / (148LL * 8);
+    // ~4 waves of the resident CTAs; chunks long enough to amortise the 3 extra planes
+    long long kchunk = (nz * tiles + 148LL * 4 * MINB - 1) / (148LL * 4 * MINB);
     static const long long kch_env = [] {   // experiment knob (tools/gpu), not a tuning path
         const char* e = std::getenv("ACS_TB_KCHUNK");
         return e ? std::atoll(e) : 0LL;
@@ -324,19 +344,60 @@ acs_status launch_tb2(const LaunchReq& r) {
     if (kchunk > nz) kchunk = nz;
     const long long chunks = (nz + kchunk - 1) / kchunk;
     dim3 grid((unsigned)((nx + TX - 1) / TX), (unsigned)((ny + TY - 1) / TY), (unsigned)chunks);
-    kern<<<grid, dim3(TX, TY, 1), G::smem, r.stream>>>(ka, map, adjx, (int)kchunk);
+    kern<<<grid, dim3(TX, TY / NY, 1), G::smem, r.stream>>>(ka, map, adjx, (int)kchunk);
     return check_launch("tb2");
 }
 
-template <class NS, class T, int TX, int TY, int PF>
+// the registered two-step schedules of a nest: configuration 0 is the default;
+// ACS_TB_CFG=<i> picks another one (an experiment knob for tools/gpu, not a tuning path)
+template <int TX, int TY, int NY, int PF, int MINB>
+struct TbCfg {};
+
+template <class NS, class T, int FORM, int... A>
+acs_status launch_tb2_cfg(const LaunchReq& r, TbCfg<A...>) {
+    return launch_tb2<NS, T, FORM, A...>(r);
+}
+
+inline int tb_cfg_env() {
+    static const int v = [] {
+        const char* e = std::getenv("ACS_TB_CFG");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+template <class NS, class T, int FORM, class C0, class... Cs>
+acs_status launch_tb2_set(const LaunchReq& r) {
+    const int want = tb_cfg_env();
+    int i = 0;
+    acs_status st = ACS_E_ARG;
+    bool done = false;
+    auto one = [&](auto cfg) {
+        if (!done && i++ == want) {
+            st = launch_tb2_cfg<NS, T, FORM>(r, cfg);
+            done = true;
+        }
+    };
+    one(C0{});
+    (one(Cs{}), ...);
+    if (!done) st = launch_tb2_cfg<NS, T, FORM>(r, C0{});
+    return st;
+}
+
+template <int TX, int TY, int NY, int PF, int MINB>
+std::string tb2_name_of(TbCfg<TX, TY, NY, PF, MINB>) {
+    return "temporal block x2 (TMA ring, register columns), tile " + std::to_string(TX) + "x" + std::to_string(TY) +
+           ", " + std::to_string(NY) + " y-cell(s) per thread, pf " + std::to_string(PF);
+}
+
+template <class NS, class T, class C0, class... Cs>
 void fill_tb2(Entry& e, int prec) {
-    e.tb2[prec][0] = &launch_tb2<NS, T, 0, TX, TY, PF>;
-    e.tb2[prec][1] = &launch_tb2<NS, T, 1, TX, TY, PF>;
-    e.tb2[prec][2] = &launch_tb2<NS, T, 2, TX, TY, PF>;
-    e.tb2[prec][3] = &launch_tb2<NS, T, 3, TX, TY, PF>;
-    e.tb2[prec][4] = &launch_tb2<NS, T, 4, TX, TY, PF>;
-    e.tb2_name[prec] = "temporal block x2 (TMA ring, register columns), tile " + std::to_string(TX) + "x" +
-                       std::to_string(TY) + " pf " + std::to_string(PF);
+    e.tb2[prec][0] = &launch_tb2_set<NS, T, 0, C0, Cs...>;
+    e.tb2[prec][1] = &launch_tb2_set<NS, T, 1, C0, Cs...>;
+    e.tb2[prec][2] = &launch_tb2_set<NS, T, 2, C0, Cs...>;
+    e.tb2[prec][3] = &launch_tb2_set<NS, T, 3, C0, Cs...>;
+    e.tb2[prec][4] = &launch_tb2_set<NS, T, 4, C0, Cs...>;
+    e.tb2_name[prec] = [](auto c) { return tb2_name_of(c); }(C0{});
     e.tb2_read = TbPlan<NS>::R;
 }
 
