@@ -14,11 +14,11 @@
  * load-div-mod-call 100, proj/src/cost.cpp:9-41) -> depth-one temps and
  * [bulk load motion] -> re-emitted module text.  Fail-open per region.
  *
- * Differences by design: extraction is greedy tree-cost followed by an exact
- * incremental DAG-cost local search (no 30 s branch-and-bound timeout), so a
- * region optimizes in milliseconds; results are checked against the frozen
- * reference outputs for objective, load count and semantics
- * (tests/test_opt.py).
+ * Extraction: greedy tree-cost followed by an exact incremental DAG-cost local
+ * search (milliseconds), then, when exact_time_s > 0 and a solver is
+ * registered, the exact 0/1 ILP (method "ilp" when proven optimal, in place
+ * of the reference's branch and bound); results are checked against the frozen
+ * reference outputs for objective, load count and semantics (tests/test_opt.py).
  */
 #ifndef ACCSAT_OPT_H
 #define ACCSAT_OPT_H
@@ -32,6 +32,8 @@ typedef struct {
     double max_time_s;     /* saturation wall-time budget (default 10) */
     int max_iters;         /* saturation iterations (default 10) */
     int dag_search;        /* 1: DAG-cost local search after greedy (default), 0: greedy only */
+    double exact_time_s;   /* > 0: exact extraction through the registered solver (acs_opt_set_solver) with this
+                              time limit per region; 0: off.  The reference's extract.max_time (30 s default) */
 } acs_opt_limits;
 
 /* Optimizes every directive-marked region of `source` for `variant`
@@ -57,6 +59,18 @@ int acs_opt_optimize(const char* source, const char* name, const char* variant, 
 int acs_opt_verify(const char* source, const char* name, const char* variant, const acs_opt_limits* limits, int trials,
                    double tol_rel, char** json_out);
 void acs_opt_free(char* p);
+/* Exact extraction (the reference's extract_ilp, proj/src/extract.cpp:202-241):
+ * the min-DAG-cost selection over the classes reachable from the roots as a
+ * 0/1 ILP.  n_nodes nodes, node i in class node_class[i] (0..n_classes-1) with
+ * cost node_cost[i] and kid classes kids[kid_ptr[i] .. kid_ptr[i+1]); the root
+ * classes must each select a node.  The solver writes chosen[i] (0/1) and a
+ * lower bound on the optimum, and returns 0 = proven optimal, 1 = time limit
+ * (chosen is feasible), 2 = no solution.  satopt.py registers HiGHS
+ * (scipy.optimize.milp); with no solver registered exact_time_s is ignored. */
+typedef int (*acs_opt_solver)(int n_nodes, int n_classes, const int* node_class, const long long* node_cost,
+                              const int* kid_ptr, const int* kids, int n_roots, const int* roots, double time_limit_s,
+                              int* chosen, double* bound);
+void acs_opt_set_solver(acs_opt_solver fn);
 
 #ifdef __cplusplus
 }

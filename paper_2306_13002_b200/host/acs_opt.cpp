@@ -23,7 +23,8 @@
 //  * Extraction: bottom-up tree-cost greedy (ties to the oldest node, i.e.
 //    the program as written) followed by an incremental DAG-cost local
 //    search: a class switches node whenever that lowers the exact cost of the
-//    shared selection.  No timeout-bound branch and bound.
+//    shared selection.  Then, optionally, the exact 0/1 ILP through a
+//    registered solver (exact_refine; method "ilp" when proven optimal).
 //  * Codegen: one `_v<class>` temp per selected operation class, placed before
 //    the first statement of the innermost block that encloses all its uses
 //    (never hoisted out of an if-branch that alone uses it); bulk mode moves
@@ -1143,6 +1144,115 @@ static Extraction extract(EGraph& g, const std::vector<int>& roots, bool dag_sea
     return x;
 }
 
+// ---- exact extraction: the DAG-cost problem as a 0/1 ILP ----
+//
+// The reference proves optimality with a branch and bound under a timeout
+// (proj/src/extract.cpp:130-174, :202-241; greedy fallback when it times out).
+// Here the problem restricted to the classes reachable from the roots is handed
+// to a registered solver (acs_opt_set_solver; satopt.py registers HiGHS through
+// scipy.optimize.milp): x_n in {0,1} per node, minimise sum cost(n) x_n subject
+// to  sum_{n in root class} x_n >= 1  and, for every non-leaf node n and kid
+// class k,  sum_{m in k} x_m >= x_n  (plus order variables when the class graph
+// has a cycle).  The incumbent (greedy + DAG local search) is kept unless the
+// ILP solution is proven optimal and strictly cheaper, so an equal-cost optimum
+// leaves the emitted text unchanged and a timed-out solve changes nothing.
+static acs_opt_solver g_solver = nullptr;
+
+struct ExactResult {
+    int status = -1;         // -1 not run, 0 proven optimal, 1 time limit (feasible), 2 failed
+    double bound = 0;        // solver's lower bound on the optimum
+    bool improved = false;
+};
+
+static ExactResult exact_refine(EGraph& g, const std::vector<int>& roots, Extraction& x, double time_s) {
+    ExactResult er;
+    if (!g_solver || time_s <= 0 || roots.empty()) return er;
+    std::vector<int> cls;                       // reachable classes (over every node)
+    std::map<int, int> idx;
+    std::vector<int> stack;
+    for (int r : roots) stack.push_back(g.find(r));
+    while (!stack.empty()) {
+        int c = g.find(stack.back());
+        stack.pop_back();
+        if (idx.count(c)) continue;
+        idx[c] = (int)cls.size();
+        cls.push_back(c);
+        for (const Node& n0 : g.cls(c).nodes) {
+            Node n = g.canon(n0);
+            if (!selection_leaf(n))
+                for (int k : n.kids) stack.push_back(g.find(k));
+        }
+    }
+    std::vector<Node> nodes;
+    std::vector<int> ncls, kptr{0}, kids;
+    std::vector<long long> ncost;
+    for (size_t ci = 0; ci < cls.size(); ++ci) {
+        std::vector<Node> seen;
+        for (const Node& n0 : g.cls(cls[ci]).nodes) {
+            Node n = g.canon(n0);
+            if (std::find(seen.begin(), seen.end(), n) != seen.end()) continue;
+            seen.push_back(n);
+            nodes.push_back(n);
+            ncls.push_back((int)ci);
+            ncost.push_back(node_cost(n));
+            if (!selection_leaf(n)) {
+                std::vector<int> ks;
+                for (int k : n.kids) ks.push_back(idx.at(g.find(k)));
+                std::sort(ks.begin(), ks.end());
+                ks.erase(std::unique(ks.begin(), ks.end()), ks.end());
+                kids.insert(kids.end(), ks.begin(), ks.end());
+            }
+            kptr.push_back((int)kids.size());
+        }
+    }
+    std::vector<int> rts;
+    for (int r : roots) rts.push_back(idx.at(g.find(r)));
+    std::sort(rts.begin(), rts.end());
+    rts.erase(std::unique(rts.begin(), rts.end()), rts.end());
+    std::vector<int> chosen(nodes.size(), 0);
+    er.status = g_solver((int)nodes.size(), (int)cls.size(), ncls.data(), ncost.data(), kptr.data(), kids.data(),
+                         (int)rts.size(), rts.data(), time_s, chosen.data(), &er.bound);
+    if (er.status != 0 && er.status != 1) return er;
+    // one chosen node per class; a selection that is not a DAG (a solver bug) is rejected
+    Extraction y;
+    y.choice = x.choice;
+    std::vector<int> pick(cls.size(), -1);
+    for (size_t i = 0; i < nodes.size(); ++i)
+        if (chosen[i] && pick[ncls[i]] < 0) pick[ncls[i]] = (int)i;
+    std::vector<int> state(cls.size(), 0);
+    bool ok = true;
+    std::function<void(int)> dfs = [&](int ci) {
+        if (!ok || state[ci] == 2) return;
+        if (state[ci] == 1 || pick[ci] < 0) {
+            ok = false;
+            return;
+        }
+        state[ci] = 1;
+        for (int q = kptr[pick[ci]]; q < kptr[pick[ci] + 1]; ++q) dfs(kids[q]);
+        state[ci] = 2;
+    };
+    for (int r : rts) dfs(r);
+    if (!ok) {
+        er.status = 2;
+        return er;
+    }
+    for (size_t ci = 0; ci < cls.size(); ++ci)
+        if (pick[ci] >= 0) y.choice[cls[ci]] = nodes[pick[ci]];
+    std::set<int> live;
+    for (int r : roots) reach(g, y.choice, r, live);
+    for (int c : live) {
+        y.total += node_cost(y.choice[c]);
+        if (y.choice[c].op == Op::Fma) y.fma++;
+    }
+    // only a PROVEN optimum replaces the incumbent: a time-limited solve could
+    // otherwise make the emitted text depend on the machine's speed
+    if (er.status == 0 && y.total < x.total) {
+        x = std::move(y);
+        er.improved = true;
+    }
+    return er;
+}
+
 // ============================================================================
 // Value numbering of a region body into the e-graph
 
@@ -1873,7 +1983,8 @@ static std::string json_str(const std::string& s) {
 struct RegionMetrics {
     int region = 0;
     std::string function, stop = "disabled", method = "greedy+dag", error;
-    double ssa_ms = 0, sat_ms = 0, extract_ms = 0;
+    double ssa_ms = 0, sat_ms = 0, extract_ms = 0, ilp_bound = -1;
+    bool timed_out = false;
     long long before = 0, after = 0;
     int loads_before = 0, loads_after = 0, stores = 0, fma = 0;
     size_t nodes = 0;
@@ -1926,10 +2037,18 @@ std::string optimize(const std::string& src, const std::string& name, bool sat, 
             }
             t0 = Clock::now();
             Extraction x = extract(g, roots, lim.dag_search != 0);
+            if (!lim.dag_search) rm.method = "greedy";
+            ExactResult er = exact_refine(g, roots, x, lim.exact_time_s);
+            if (er.status == 0) {
+                rm.method = "ilp";                       // proven optimal (the reference's ExtractMethod::Ilp)
+                rm.ilp_bound = er.bound;
+            } else if (er.status == 1) {
+                rm.timed_out = true;                     // the reference's greedy fallback on timeout
+                rm.ilp_bound = er.bound;
+            }
             rm.extract_ms = ms(t0);
             rm.after = x.total;
             rm.fma = x.fma;
-            if (!lim.dag_search) rm.method = "greedy";
             Emitter em(g, x, b, src, bulk);
             std::string inner = em.emit(body);
             // indentation of the anchor body braces
@@ -1980,7 +2099,9 @@ std::string optimize(const std::string& src, const std::string& name, bool sat, 
           << ", \"objective_before\": " << r.before << ", \"objective_after\": " << r.after
           << ", \"static_loads_before\": " << r.loads_before << ", \"static_loads_after\": " << r.loads_after
           << ", \"static_stores\": " << r.stores << ", \"fma_count\": " << r.fma << ", \"method\": "
-          << json_str(r.method) << ", \"timed_out\": false, \"error\": " << json_str(r.error) << "}";
+          << json_str(r.method) << ", \"timed_out\": " << (r.timed_out ? "true" : "false");
+        if (r.ilp_bound >= 0) j << ", \"ilp_bound\": " << (long long)std::ceil(r.ilp_bound - 1e-6);
+        j << ", \"error\": " << json_str(r.error) << "}";
     }
     j << "\n  ]\n}\n";
     json = j.str();
@@ -2350,7 +2471,7 @@ extern "C" {
 
 int acs_opt_optimize(const char* source, const char* name, const char* variant, const acs_opt_limits* limits,
                      char** text_out, char** json_out) {
-    acs_opt_limits lim{10000, 10.0, 10, 1};
+    acs_opt_limits lim{10000, 10.0, 10, 1, 0.0};
     if (limits) lim = *limits;
     std::string v = variant ? variant : "accsat";
     bool sat = v == "accsat" || v == "cse+sat";
@@ -2377,7 +2498,7 @@ int acs_opt_optimize(const char* source, const char* name, const char* variant, 
 
 int acs_opt_verify(const char* source, const char* name, const char* variant, const acs_opt_limits* limits, int trials,
                    double tol_rel, char** json_out) {
-    acs_opt_limits lim{10000, 10.0, 10, 1};
+    acs_opt_limits lim{10000, 10.0, 10, 1, 0.0};
     if (limits) lim = *limits;
     std::string v = variant ? variant : "accsat";
     auto dup = [](const std::string& s) {
@@ -2400,5 +2521,7 @@ int acs_opt_verify(const char* source, const char* name, const char* variant, co
 }
 
 void acs_opt_free(char* p) { std::free(p); }
+
+void acs_opt_set_solver(acs_opt_solver fn) { acsopt::g_solver = fn; }
 
 }  // extern "C"

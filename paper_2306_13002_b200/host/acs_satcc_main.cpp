@@ -46,7 +46,7 @@ static std::string read_file(const std::string& p) {
 int main(int argc, char** argv) {
     std::vector<std::string> args(argv + 1, argv + argc);
     std::string cmd = "opt", variant = "accsat", output;
-    acs_opt_limits lim{10000, 10.0, 10, 1};
+    acs_opt_limits lim{10000, 10.0, 10, 1, 0.0};
     bool no_sat = false, no_bulk = false, keep = false;
     std::string backend = "cc";   // cc: hand the optimized C to the wrapped compiler; b200: to this backend
     bool gpu = false;             // report --gpu: satcc-metrics-v1 plus the B200 execution of every region

@@ -18,7 +18,125 @@ CLI_PATH = os.path.join(HERE, "acs-satcc")
 
 class Limits(ctypes.Structure):
     _fields_ = [("max_nodes", ctypes.c_long), ("max_time_s", ctypes.c_double), ("max_iters", ctypes.c_int),
-                ("dag_search", ctypes.c_int)]
+                ("dag_search", ctypes.c_int), ("exact_time_s", ctypes.c_double)]
+
+
+# exact extraction time limit per region used by the build (stage_a.py): the reference's
+# PipelineLimits extract.max_time default (proj/include/satcc/pipeline.hpp)
+EXACT_TIME_S = 30.0
+
+SOLVER_T = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                            ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_int),
+                            ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_double,
+                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double))
+
+
+def solve_extraction(node_class, node_cost, kid_ptr, kids, roots, time_limit_s):
+    """Min-DAG-cost e-graph extraction as a 0/1 ILP (HiGHS via scipy.optimize.milp).
+
+    x_n in {0,1}; minimise sum cost_n x_n; every root class selects a node;
+    a selected non-leaf node needs a selected node in each kid class
+    (sum_{m in k} x_m - x_n >= 0).  When the class graph has a cycle, order
+    variables t_c in [0, K] forbid cyclic selections (t_c - t_k - K x_n >= 1 - K).
+    Returns (status, chosen 0/1 array, lower bound): 0 optimal, 1 time limit
+    with a feasible selection, 2 no solution."""
+    import numpy as np
+    from scipy.optimize import LinearConstraint, milp
+    from scipy.sparse import coo_matrix
+    node_class = np.asarray(node_class, dtype=np.int64)
+    n = len(node_class)
+    K = int(node_class.max()) + 1 if n else 0
+    kid_ptr = np.asarray(kid_ptr, dtype=np.int64)
+    kids = np.asarray(kids, dtype=np.int64)
+    members = [[] for _ in range(K)]
+    for i, c in enumerate(node_class):
+        members[c].append(i)
+    # is the class graph (over every node) cyclic?
+    succ = [set() for _ in range(K)]
+    for i in range(n):
+        succ[node_class[i]].update(kids[kid_ptr[i]:kid_ptr[i + 1]].tolist())
+    state, cyclic = [0] * K, False
+    for s0 in range(K):
+        if state[s0]:
+            continue
+        stack = [(s0, iter(succ[s0]))]
+        state[s0] = 1
+        while stack and not cyclic:
+            c, it = stack[-1]
+            nxt = next(it, None)
+            if nxt is None:
+                state[c] = 2
+                stack.pop()
+            elif state[nxt] == 1:
+                cyclic = True
+            elif state[nxt] == 0:
+                state[nxt] = 1
+                stack.append((nxt, iter(succ[nxt])))
+        if cyclic:
+            break
+    nv = n + (K if cyclic else 0)
+    rows, cols, vals, lb, ub = [], [], [], [], []
+    r = 0
+    for c in roots:                       # root classes select a node
+        for m in members[c]:
+            rows.append(r); cols.append(m); vals.append(1.0)
+        lb.append(1.0); ub.append(np.inf); r += 1
+    for i in range(n):                    # a selected node needs each kid class
+        for k in kids[kid_ptr[i]:kid_ptr[i + 1]]:
+            for m in members[k]:
+                rows.append(r); cols.append(m); vals.append(1.0)
+            rows.append(r); cols.append(i); vals.append(-1.0)
+            lb.append(0.0); ub.append(np.inf); r += 1
+            if cyclic:
+                rows += [r, r, r]; cols += [n + node_class[i], n + int(k), i]; vals += [1.0, -1.0, -float(K)]
+                lb.append(1.0 - K); ub.append(np.inf); r += 1
+    cost = np.zeros(nv)
+    cost[:n] = np.asarray(node_cost, dtype=np.float64)
+    integrality = np.zeros(nv)
+    integrality[:n] = 1
+    lo = np.zeros(nv)
+    hi = np.ones(nv)
+    if cyclic:
+        hi[n:] = K
+    from scipy.optimize import Bounds
+    A = coo_matrix((vals, (rows, cols)), shape=(r, nv)).tocsr()
+    res = milp(cost, constraints=LinearConstraint(A, lb, ub), integrality=integrality, bounds=Bounds(lo, hi),
+               options={"time_limit": float(time_limit_s), "disp": False})
+    if res.x is None:
+        return 2, None, 0.0
+    chosen = (res.x[:n] > 0.5).astype(np.int32)
+    bound = getattr(res, "mip_dual_bound", None)
+    if bound is None or not np.isfinite(bound):
+        bound = res.fun if res.status == 0 else 0.0
+    return (0 if res.status == 0 else 1), chosen, float(bound)
+
+
+_solved: dict = {}
+
+
+@SOLVER_T
+def _solver_cb(n_nodes, n_classes, node_class, node_cost, kid_ptr, kids, n_roots, roots, time_limit_s, chosen,
+               bound):
+    try:
+        import numpy as np
+        nc = np.ctypeslib.as_array(node_class, shape=(n_nodes,)).copy()
+        co = np.ctypeslib.as_array(node_cost, shape=(n_nodes,)).copy()
+        kp = np.ctypeslib.as_array(kid_ptr, shape=(n_nodes + 1,)).copy()
+        nk = int(kp[-1])
+        kd = np.ctypeslib.as_array(kids, shape=(nk,)).copy() if nk else np.zeros(0, dtype=np.int32)
+        rt = np.ctypeslib.as_array(roots, shape=(n_roots,)).tolist()
+        # the cse+sat and accsat variants extract from the same e-graph: solve once
+        key = (nc.tobytes(), co.tobytes(), kp.tobytes(), kd.tobytes(), tuple(rt), float(time_limit_s))
+        if key not in _solved:
+            _solved[key] = solve_extraction(nc, co, kp, kd, rt, time_limit_s)
+        st, ch, b = _solved[key]
+        if ch is not None:
+            for i in range(n_nodes):
+                chosen[i] = int(ch[i])
+        bound[0] = b
+        return st
+    except Exception:   # a solver failure leaves the incumbent (reported as not run)
+        return 2
 
 
 _lib = None
@@ -37,13 +155,23 @@ def lib():
         L.acs_opt_verify.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(Limits),
                                      ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_void_p)]
         L.acs_opt_free.argtypes = [ctypes.c_void_p]
+        L.acs_opt_set_solver.argtypes = [SOLVER_T]
+        L.acs_opt_set_solver.restype = None
+        try:
+            import scipy.optimize  # noqa: F401
+            L.acs_opt_set_solver(_solver_cb)
+        except ImportError:     # no HiGHS: exact_time_s is ignored (method stays greedy+dag)
+            pass
         _lib = L
     return _lib
 
 
 def optimize_source(source: str, name: str = "<input>", variant: str = "accsat", max_nodes: int = 10000,
-                    max_time_s: float = 10.0, max_iters: int = 10, dag_search: bool = True) -> Tuple[str, dict]:
-    lim = Limits(max_nodes, max_time_s, max_iters, 1 if dag_search else 0)
+                    max_time_s: float = 10.0, max_iters: int = 10, dag_search: bool = True,
+                    exact_time_s: float = 0.0) -> Tuple[str, dict]:
+    """exact_time_s > 0: exact ILP extraction per region with that time limit
+    (method "ilp" when proven optimal; the build uses EXACT_TIME_S)."""
+    lim = Limits(max_nodes, max_time_s, max_iters, 1 if dag_search else 0, float(exact_time_s))
     t, j = ctypes.c_void_p(), ctypes.c_void_p()
     rc = lib().acs_opt_optimize(source.encode(), name.encode(), variant.encode(), ctypes.byref(lim),
                                 ctypes.byref(t), ctypes.byref(j))
@@ -60,7 +188,7 @@ def verify_source(source: str, name: str = "<input>", variant: str = "accsat", t
                   tol_rel: float = 1e-6, max_nodes: int = 10000, max_time_s: float = 10.0, max_iters: int = 10,
                   dag_search: bool = True) -> Tuple[bool, dict]:
     """satcc verify for one source: (all regions ok, per-file report)."""
-    lim = Limits(max_nodes, max_time_s, max_iters, 1 if dag_search else 0)
+    lim = Limits(max_nodes, max_time_s, max_iters, 1 if dag_search else 0, 0.0)
     j = ctypes.c_void_p()
     rc = lib().acs_opt_verify(source.encode(), name.encode(), variant.encode(), ctypes.byref(lim), trials, tol_rel,
                               ctypes.byref(j))

@@ -55,12 +55,17 @@ def test_registry_metrics_match_stage_a_and_reference(kid):
     assert k.info["scalars"] == [s.name for s in spec.scalars]
     order = ["original", "cse", "cse+bulk", "cse+sat", "accsat"]
     for vi, v in enumerate(order[1:], start=1):
-        for reg in (stage_a.metrics(spec.nest, v)["regions"][spec.region],
-                    json.load(open(os.path.join(nests.GOLDEN_DIR, f"{spec.nest}.{v}.json")))["regions"][spec.region]):
+        ours = stage_a.metrics(spec.nest, v)["regions"][spec.region]
+        ref = json.load(open(os.path.join(nests.GOLDEN_DIR, f"{spec.nest}.{v}.json")))["regions"][spec.region]
+        assert ours["objective_after"] <= ref["objective_after"]
+        for reg in (ours, ref):
             assert reg["function"] == spec.function
             assert k.info["static_loads"][0] == reg["static_loads_before"]
             assert k.info["static_loads"][vi] == reg["static_loads_after"], (v, k.info["static_loads"])
-            assert k.info["fma_count"][vi] == reg["fma_count"], (v, k.info["fma_count"])
+            # the FMA count is the extraction's: equal to the reference's unless our exact
+            # extraction found a strictly cheaper selection (swim calc2, pdv, zsolve)
+            if reg is ours or ours["objective_after"] == ref["objective_after"]:
+                assert k.info["fma_count"][vi] == reg["fma_count"], (v, k.info["fma_count"])
 
 
 def test_build_reads_stage_a_not_reference_goldens():

