@@ -239,6 +239,22 @@ acs_status acs_wait_ctr(const uint64_t* flag_a, const uint64_t* flag_b, const ui
 acs_status acs_launch_steps(const acs_kernel* k, acs_variant variant, const acs_array* arrays, int n_arrays,
                             const acs_scalar* scalars, int n_scalars, int nsteps, int blocked, void* cuda_stream,
                             int* latest);
+
+/* Two time steps of a 3-level leapfrog nest (wave4: un = f(u, up, vel2), the
+ * time loop rotating up <- u <- un) in ONE launch (temporal blocking,
+ * kernels/tbwave.cuh).  Step 1 is written to `un` as a single step would;
+ * step 2 goes to `un2`, a fourth buffer of un's dims / strides (the loop's
+ * free buffer, up, is still read by neighbouring tiles' step 1).  After the
+ * call the loop's state is up = un, u = un2 — the same values two
+ * acs_launch calls with the rotation produce, bit for bit, provided every
+ * rotating buffer (u, up, un, un2) carries the same fixed boundary (the
+ * cells outside the iteration space, never written by the nest).  Replaces two
+ * iterations of the nest's time loop (the reference runs one step per
+ * eval_region, proj/src/interp.cpp:266-270).  ACS_E_NO_KERNEL when the nest
+ * or precision has no two-step kernel; ACS_E_LAYOUT when the TMA cannot
+ * describe the arrays. */
+acs_status acs_launch_leapfrog2(const acs_kernel* k, acs_variant variant, const acs_array* arrays, int n_arrays,
+                                const acs_scalar* scalars, int n_scalars, const acs_array* un2, void* cuda_stream);
 /* eval_region for HOST arrays (row-major, the reference layout; `data` =
  * host pointers): uploads every array, runs the whole nest with the DEFAULT
  * schedule, downloads every array the nest stores, synchronously.  The call a

@@ -213,6 +213,20 @@ class Kernel:
                  _stream_handle(stream), ctypes.byref(latest)), f"acs_launch_steps({self.kernel_id})")
         return names[latest.value]
 
+    def launch_leapfrog2(self, arrays: Dict[str, object], un2, scalars: Dict[str, float], variant: str = "accsat",
+                         stream=None) -> None:
+        """acs_launch_leapfrog2: two steps of a 3-level leapfrog nest (wave4) in
+        one launch: step 1 into arrays["un"], step 2 into `un2` (a fourth buffer
+        of un's layout).  Afterwards the time loop's up is un, its u is un2."""
+        descs, sc = self._pack(arrays, scalars)
+        extra = describe("un2", un2)
+        f = lib().acs_launch_leapfrog2
+        f.restype = ctypes.c_int
+        f.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(AcsArray), ctypes.c_int, ctypes.POINTER(AcsScalar),
+                      ctypes.c_int, ctypes.POINTER(AcsArray), ctypes.c_void_p]
+        _check(f(self.handle, VARIANTS[variant], descs, len(arrays), sc, len(scalars), ctypes.byref(extra),
+                 _stream_handle(stream)), f"acs_launch_leapfrog2({self.kernel_id}, {variant})")
+
     def tune(self, arrays, scalars, variant: str = "accsat", reps: int = 3, stream=None):
         """acs_tune: times every registered schedule slot on these arrays and
         makes the fastest the default for this variant.  Returns

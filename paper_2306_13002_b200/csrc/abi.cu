@@ -546,6 +546,26 @@ acs_status acs_launch_steps(const acs_kernel* k, acs_variant variant, const acs_
     return ACS_OK;
 }
 
+acs_status acs_launch_leapfrog2(const acs_kernel* k, acs_variant variant, const acs_array* arrays, int n_arrays,
+                                const acs_scalar* scalars, int n_scalars, const acs_array* un2, void* cuda_stream) {
+    if (!k || !arrays || n_arrays < 1 || !un2 || (int)variant < 0 || (int)variant > 4) {
+        set_error("acs_launch_leapfrog2: the nest's arrays, a fourth buffer un2, a variant 0..4");
+        return ACS_E_ARG;
+    }
+    const Entry* e = reinterpret_cast<const Entry*>(k);
+    const int prec = precision_of(arrays, n_arrays);
+    LaunchFn tb = e->tb2[prec][variant];
+    if (!tb || e->arrays.size() != 4) {
+        set_error(e->kernel_id + ": no two-step leapfrog kernel registered" + (prec ? " (fp32)" : " (fp64)"));
+        return ACS_E_NO_KERNEL;
+    }
+    std::vector<acs_array> all(arrays, arrays + n_arrays);
+    all.push_back(*un2);
+    all.back().name = "un2";
+    LaunchReq r{all.data(), (int)all.size(), scalars, n_scalars, static_cast<cudaStream_t>(cuda_stream)};
+    return tb(r);
+}
+
 acs_status acs_eval_host(const acs_kernel* k, acs_variant variant, const acs_array* host, int n_arrays,
                          const acs_scalar* scalars, int n_scalars) {
     if (!k || (n_arrays > 0 && !host) || (n_scalars > 0 && !scalars)) {

@@ -1,6 +1,7 @@
 // Registration of the wave4 nest functions (generated bodies: gen/wave4.cuh).
 #include "registry.hpp"
 #include "kernels/march.cuh"
+#include "kernels/tbwave.cuh"
 #include "gen/wave4.cuh"
 
 namespace acs {
@@ -23,6 +24,9 @@ void register_wave4() {
         fill_march<gen::wave4_f32, float, 0, 64, 8, 64, 2, 4>(e, 1);
         fill_march<gen::wave4_f32, float, 0, 64, 16, 16, 16, 2, 4>(e, 1);
         fill_march<gen::wave4_f32, float, 0, 32, 16, 32, 4, 3>(e, 1);
+        // two leapfrog steps per launch (kernels/tbwave.cuh, acs_launch_leapfrog2), fp32 config
+        fill_tbw<gen::wave4_f32, float, gen::wave4_f32::ARR_u, gen::wave4_f32::ARR_up, gen::wave4_f32::ARR_un,
+                 gen::wave4_f32::ARR_vel2, 32, 16, 2, 3>(e, 1);
         register_entry(&e);
     }
 }

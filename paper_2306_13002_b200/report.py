@@ -96,7 +96,7 @@ def _to_host(t):
 def report(path: str, variant: str = "accsat", gpu: bool = True, size=None) -> Dict:
     src = open(path).read()
     name = os.path.basename(path)
-    _, meta = satopt.optimize_source(src, path, variant)
+    _, meta = satopt.optimize_source(src, path, variant, exact_time_s=satopt.EXACT_TIME_S)
     if gpu:
         registered = set(backend.kernel_ids())
         for r in meta["regions"]:

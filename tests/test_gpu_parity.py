@@ -388,3 +388,40 @@ def test_temporal_blocking_equals_step_by_step(size, nsteps, variant):
     latest = k.launch_steps(dev, dict(w.scalars), variant, nsteps, blocked=True)
     got = to_host(dev[latest])
     assert bitwise_equal(got, g[newest]), f"{size} x{nsteps}"
+
+
+@pytest.mark.parametrize("size", [(6, 7, 13), (21, 9, 70), (33, 47, 130), (70, 40, 37)])
+@pytest.mark.parametrize("nsteps", [2, 4, 6])
+@pytest.mark.parametrize("variant", ["original", "accsat"])
+def test_wave4_leapfrog2_equals_step_by_step(size, nsteps, variant):
+    """acs_launch_leapfrog2 (two wave4 fp32 steps per launch, kernels/tbwave.cuh:
+    step 1 to un, step 2 to a fourth buffer) rotated like the time loop gives the
+    newest u and up of the step-by-step oracle bit for bit.  Precondition of the
+    two-step launch (as for Jacobi's): every rotating buffer carries the same
+    fixed boundary (the time loop's boundary condition) — set here from u's."""
+    torch = _torch()
+    kid = "wave4.c:wave4:0"
+    spec = nests.kernel(kid)
+    w = nests.workload(kid, size, dtype="f32")
+    ins = nests.make_inputs(w)
+    sc = w.scalars
+    inner = np.zeros(ins["u"].shape, dtype=bool)
+    inner[int(sc["kbeg"]):int(sc["kend"]), 2:int(sc["ny"]) - 2, 2:int(sc["nx"]) - 2] = True
+    for n in ("up", "un"):
+        ins[n][~inner] = ins["u"][~inner]
+    g = {n: a.copy() for n, a in ins.items()}
+    for t in range(nsteps):
+        roles = nests.role_buffers(spec.nest, list(g), t)
+        oracle_cpu.run(spec, {p: g[b] for p, b in roles.items()}, w.scalars, variant, fma=variant in SAT, f32=True)
+    roles = nests.role_buffers(spec.nest, list(g), nsteps)
+    k = backend.Kernel.lookup(kid)
+    dev = {n: to_device(k, n, a) for n, a in ins.items()}
+    x = to_device(k, "un", ins["un"])        # the fourth buffer: any content (un's layout)
+    bufs = {"u": dev["u"], "up": dev["up"], "un": dev["un"], "x": x}
+    for _ in range(nsteps // 2):
+        k.launch_leapfrog2({"u": bufs["u"], "up": bufs["up"], "un": bufs["un"], "vel2": dev["vel2"]}, bufs["x"],
+                           dict(w.scalars), variant)
+        bufs = {"u": bufs["x"], "up": bufs["un"], "un": bufs["up"], "x": bufs["u"]}
+    assert bitwise_equal(to_host(bufs["u"]), g[roles["u"]]), f"{size} x{nsteps}: u"
+    assert bitwise_equal(to_host(bufs["up"]), g[roles["up"]]), f"{size} x{nsteps}: up"
+    assert bitwise_equal(to_host(dev["vel2"]), ins["vel2"])
