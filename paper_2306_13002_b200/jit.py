@@ -52,6 +52,44 @@ class JitError(RuntimeError):
     pass
 
 
+def offload_regions(mod: ks.Module, fn: ks.Function, regions: List[ks.Region]) -> List[ks.Region]:
+    """The regions of `fn` the hand-off can run on the B200.  A function that is
+    only its nest goes whole (its body becomes one launch); otherwise each
+    region is replaced IN PLACE by a launch and the rest of the function —
+    enclosing time loops included — stays on the host, passing the enclosing
+    loop indices and the live-in locals as scalars (lowering.region_view).  A
+    region whose scalar assignments are read elsewhere in the function (a
+    live-out) stays on the CPU (fail-open)."""
+    from . import lowering
+    if len(regions) == 1 and offloadable(fn, regions):
+        return regions
+    out = []
+    for r in regions:
+        try:
+            lowering.region_view(mod, fn, r)
+        except lowering.LowerError:
+            continue
+        top = r.marked_loops[0]
+        _, writes = lowering._stmt_reads_writes(top)
+        writes -= {l.loop_var for l in r.marked_loops}
+        inside = {id(t) for t in lowering._walk_stmts(top)}
+        outside_reads = set()
+        for t in lowering._walk_stmts(fn.body):
+            if id(t) in inside or t.kind == "block":
+                continue
+            rd, _ = lowering._stmt_reads_writes(ks.Stmt(t.kind, lhs=t.lhs, rhs=t.rhs, cond=t.cond, call=t.call,
+                                                         names=t.names))
+            outside_reads |= rd
+        if writes & outside_reads:
+            continue
+        out.append(r)
+    return out
+
+
+def ns_name(fn: ks.Function, r: ks.Region, whole: bool) -> str:
+    return fn.name if whole else f"{fn.name}_r{r.index}"
+
+
 def offloadable(fn: ks.Function, regions: List[ks.Region]) -> bool:
     """The function body is declarations plus the outermost loops of its
     regions (so replacing it by the region launches keeps its semantics)."""
@@ -93,12 +131,18 @@ def build(c_path: str, cache_dir: Optional[str] = None) -> Tuple[str, List[str]]
     by_fn: Dict[str, List[ks.Region]] = {}
     for r in regions:
         by_fn.setdefault(r.function.name, []).append(r)
-    fns = [f for f in mod.functions if f.name in by_fn and offloadable(f, by_fn[f.name])]
-    if not fns:
+    plan = []          # (function, region, struct name)
+    for f in mod.functions:
+        if f.name not in by_fn:
+            continue
+        regs = offload_regions(mod, f, by_fn[f.name])
+        whole = len(by_fn[f.name]) == 1 and offloadable(f, by_fn[f.name])
+        plan += [(f, r, ns_name(f, r, whole)) for r in regs]
+    if not plan:
         raise JitError(f"{name}: no region function to offload")
     out = os.path.join(cache_dir or CACHE, f"{stem}_{_digest(src)}")
     lib = os.path.join(out, "libaccsat_jit.so")
-    ids = [f"{name}:{r.function.name}:{r.index}" for f in fns for r in by_fn[f.name]]
+    ids = [f"{name}:{f.name}:{r.index}" for f, r, _ in plan]
     if os.path.exists(lib):
         return lib, ids
     os.makedirs(out, exist_ok=True)
@@ -108,21 +152,18 @@ def build(c_path: str, cache_dir: Optional[str] = None) -> Tuple[str, List[str]]
         sources[v] = text
     parts = [f"// GENERATED by paper_2306_13002_b200/jit.py from {name}", "#pragma once",
              "namespace acs { namespace gen {"]
-    for f in fns:
-        if len(by_fn[f.name]) != 1:
-            raise JitError(f"{name}:{f.name}: one region per function (got {len(by_fn[f.name])})")
-        txt, _ = lowering.gen_function(stem, f.name, sources=sources)
+    for f, r, nsn in plan:
+        txt, _ = lowering.gen_function(stem, f.name, sources=sources, region_index=r.index, ns_name=nsn)
         parts.append(txt)
     parts.append("}}  // namespace acs::gen")
     with open(os.path.join(out, "gen_jit.cuh"), "w") as fh:
         fh.write("\n".join(parts) + "\n")
     reg = ["// GENERATED by paper_2306_13002_b200/jit.py", '#include "registry.hpp"', '#include "kernels/march.cuh"',
            '#include "gen_jit.cuh"', "namespace acs {", "void register_jit() {"]
-    for f in fns:
-        r = by_fn[f.name][0]
+    for f, r, nsn in plan:
         reg += ["    {", "        static Entry e;", f'        e.kernel_id = "{name}:{f.name}:{r.index}";',
-                f'        e.function = "{f.name}";', f'        describe<gen::{f.name}>(e, "{name}", {r.index});',
-                f"        fill_default<gen::{f.name}, double>(e);", "        register_entry(&e);", "    }"]
+                f'        e.function = "{f.name}";', f'        describe<gen::{nsn}>(e, "{name}", {r.index});',
+                f"        fill_default<gen::{nsn}, double>(e);", "        register_entry(&e);", "    }"]
     reg += ["}", "}  // namespace acs"]
     with open(os.path.join(out, "jit_reg.cu"), "w") as fh:
         fh.write("\n".join(reg) + "\n")
@@ -177,24 +218,36 @@ def stub_source(src: str, name: str, variant: str) -> Tuple[str, List[str]]:
     spans = _function_bodies(src)
     dt = {"double": "ACS_F64", "int": "ACS_I32"}
     edits, ids = [], []
-    for f in mod.functions:
-        if f.name not in by_fn or not offloadable(f, by_fn[f.name]) or len(by_fn[f.name]) != 1:
-            continue
-        kid = f"{name}:{f.name}:{by_fn[f.name][0].index}"
-        params = lowering.region_params(mod, f)        # the function's own, then the file's globals
+
+    def launch(f, r, ind):
+        kid = f"{name}:{f.name}:{r.index}"
+        # the function's own parameters, the file's globals, then (in-place regions) the
+        # enclosing loop indices and live-in locals
+        params = lowering.region_params(mod, f, r)
         arrs = [p for p in params if p.dims]
         scs = [p for p in params if not p.dims]
         a_init = ", ".join("{" + f'"{p.name}", {dt[p.ty]}, {len(p.dims)}, {{{", ".join(str(d) for d in p.dims)}}}, '
                            f"{{0}}, (void*){p.name}" + "}" for p in arrs)
         s_init = ", ".join("{" + f'"{p.name}", {1 if p.ty == "int" else 0}, '
                            f'{p.name if p.ty == "int" else 0}, {p.name if p.ty != "int" else 0.0}' + "}" for p in scs)
-        body = ["{", f"    /* {f.name}: offloaded to the B200 by paper_2306_13002_b200/jit.py ({variant}) */"]
-        body.append(f"    acs_array a_[{max(1, len(arrs))}] = {{{a_init}}};")
-        body.append(f"    acs_scalar s_[{max(1, len(scs))}] = {{{s_init}}};")
-        body.append(f'    acs_jit_run_("{kid}", {VARIANT_ENUM[variant]}, a_, {len(arrs)}, s_, {len(scs)});')
-        body.append("}")
-        edits.append((spans[f.name], "\n".join(body)))
+        body = ["{", f"{ind}/* {kid}: offloaded to the B200 by paper_2306_13002_b200/jit.py ({variant}) */"]
+        body.append(f"{ind}acs_array a_[{max(1, len(arrs))}] = {{{a_init}}};")
+        body.append(f"{ind}acs_scalar s_[{max(1, len(scs))}] = {{{s_init}}};")
+        body.append(f'{ind}acs_jit_run_("{kid}", {VARIANT_ENUM[variant]}, a_, {len(arrs)}, s_, {len(scs)});')
         ids.append(kid)
+        return body
+
+    for f in mod.functions:
+        if f.name not in by_fn:
+            continue
+        if len(by_fn[f.name]) == 1 and offloadable(f, by_fn[f.name]):
+            edits.append((spans[f.name], "\n".join(launch(f, by_fn[f.name][0], "    ") + ["}"])))
+            continue
+        for r in offload_regions(mod, f, by_fn[f.name]):
+            top = r.marked_loops[0]
+            ls = src.rfind("\n", 0, top.beg) + 1
+            ind = src[ls:top.beg] if src[ls:top.beg].strip() == "" else ""
+            edits.append(((top.beg, top.end), ("\n" + ind).join(launch(f, r, "    ") + ["}"])))
     out = src
     for (b, e), text in sorted(edits, key=lambda x: -x[0][0]):
         out = out[:b] + text + out[e:]

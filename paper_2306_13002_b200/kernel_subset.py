@@ -40,6 +40,8 @@ class Tok:
     kind: str   # 'int' 'float' 'ident' 'kw' 'op' 'pragma' 'end'
     text: str
     line: int
+    pos: int = 0     # byte span in the source
+    end: int = 0
 
 
 def lex(src: str) -> List[Tok]:
@@ -62,7 +64,7 @@ def lex(src: str) -> List[Tok]:
             text = src[pos:nl]
             if not re.match(r"#\s*pragma\b", text):
                 raise SyntaxError(f"{line}: only #pragma preprocessor lines are supported")
-            toks.append(Tok("pragma", text, line))
+            toks.append(Tok("pragma", text, line, pos, nl))
             line += text.count("\n")
             pos = nl
             continue
@@ -74,12 +76,12 @@ def lex(src: str) -> List[Tok]:
         if kind in ("ws", "lcomment", "bcomment"):
             pass
         elif kind == "ident" and text in KEYWORDS:
-            toks.append(Tok("kw", text, line))
+            toks.append(Tok("kw", text, line, pos, m.end()))
         else:
-            toks.append(Tok(kind, text, line))
+            toks.append(Tok(kind, text, line, pos, m.end()))
         line += text.count("\n")
         pos = m.end()
-    toks.append(Tok("end", "", line))
+    toks.append(Tok("end", "", line, n, n))
     return toks
 
 
@@ -120,6 +122,9 @@ class Stmt:
     stmts: List["Stmt"] = field(default_factory=list)
     # call
     call: Optional[Expr] = None
+    # byte span in the source, pragma lines included (beg, end)
+    beg: int = -1
+    end: int = -1
 
 
 @dataclass
@@ -253,6 +258,7 @@ class _Parser:
         self.expect("{")
         s = Stmt("block")
         while True:
+            b0 = self.cur().pos
             prag = self.pragmas()
             if self.check("}"):
                 if prag:
@@ -260,11 +266,19 @@ class _Parser:
                 break
             st = self.stmt()
             st.pragmas = prag + st.pragmas
+            if prag:
+                st.beg = b0
             s.stmts.append(st)
         self.expect("}")
         return s
 
     def stmt(self) -> Stmt:
+        b0 = self.cur().pos
+        s = self._stmt()
+        s.beg, s.end = b0, self.t[self.p - 1].end
+        return s
+
+    def _stmt(self) -> Stmt:
         prag = self.pragmas()
         c = self.cur()
         if c.kind == "op" and c.text == "{":

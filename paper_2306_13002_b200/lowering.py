@@ -963,17 +963,117 @@ def global_params(mod: ks.Module) -> List[ks.Param]:
     return out
 
 
-def region_params(mod: ks.Module, fn: ks.Function) -> List[ks.Param]:
+def _walk_stmts(s: Optional[ks.Stmt]):
+    if s is None:
+        return
+    yield s
+    for c in ks.children(s):
+        yield from _walk_stmts(c)
+
+
+def _stmt_reads_writes(s: ks.Stmt) -> Tuple[set, set]:
+    """Scalar names a statement subtree reads / assigns (loop headers included)."""
+    reads, writes = set(), set()
+    for t in _walk_stmts(s):
+        if t.kind == "assign":
+            if t.lhs.kind == "var":
+                writes.add(t.lhs.op)           # compound forms are desugared: x = x + e reads x
+            else:
+                for k in t.lhs.kids:
+                    reads |= ks_vars(k)
+            reads |= ks_vars(t.rhs)
+        elif t.kind == "decl":
+            for name, dims, init in t.names:
+                reads |= ks_vars(init)
+                if init is not None:
+                    writes.add(name)
+        for e in (t.cond, t.call):
+            reads |= ks_vars(e)
+    return reads, writes
+
+
+def simple_nest_function(fn: ks.Function, region: ks.Region) -> bool:
+    """The function body is declarations plus the region's loops, all marked
+    (the shape every benchmark nest has: the region IS the function)."""
+    if len(region.marked_loops) != len(region.loops):
+        return False
+
+    def ok(stmts):
+        for s in stmts:
+            if s.kind in ("decl", "empty") or s is region.loops[0]:
+                continue
+            if s.kind == "block" and ok(s.stmts):
+                continue
+            return False
+        return True
+    return ok(fn.body.stmts if fn.body.kind == "block" else [fn.body])
+
+
+def region_view(mod: ks.Module, fn: ks.Function, region: ks.Region) -> Tuple[ks.Function, ks.Region, List[ks.Param]]:
+    """The region as a function of its own: the marked nest only, with the
+    scalars it takes from the enclosing function as implicit parameters —
+    the variables of unmarked loops ENCLOSING the nest (a time loop around it
+    runs on the host and passes its index per launch) and function locals the
+    nest reads but never assigns (live-ins).  Returns (function, region,
+    implicit params).  Unmarked loops must enclose the marked ones
+    (the reference's iteration space, proj/src/ast.cpp:333-398)."""
+    marked = region.marked_loops
+    n_un = len(region.loops) - len(marked)
+    if region.loops[n_un:] != marked:
+        raise LowerError(f"{fn.name}: an unmarked loop between marked loops of the region")
+    top = marked[0]
+    decl_ty: Dict[str, str] = {}
+    for t in _walk_stmts(fn.body):
+        if t.kind == "decl":
+            for name, dims, init in t.names:
+                if not dims:
+                    decl_ty[name] = t.ty
+    known = {p.name for p in fn.params} | {p.name for p in global_params(mod)}
+    implicit: List[ks.Param] = []
+    for l in region.loops[:n_un]:
+        if l.loop_var in known:
+            raise LowerError(f"{fn.name}: enclosing loop variable '{l.loop_var}' is a parameter")
+        implicit.append(ks.Param("int", l.loop_var, []))
+    reads, writes = _stmt_reads_writes(top)
+    inner_vars = {l.loop_var for l in marked}
+    taken = {p.name for p in implicit}
+    for name in sorted(reads - writes - inner_vars - known - taken):
+        if name in decl_ty:
+            implicit.append(ks.Param(decl_ty[name], name, []))
+    # the nest's own temporaries stay local declarations of the view
+    drop = {p.name for p in implicit}
+    decls = []
+    for name, ty in decl_ty.items():
+        if name not in drop and name not in inner_vars and name in (reads | writes):
+            decls.append(ks.Stmt("decl", ty=ty, names=[(name, [], None)]))
+    body = ks.Stmt("block", stmts=decls + [top])
+    vfn = ks.Function(fn.name, list(fn.params) + implicit, body)
+    vreg = ks.Region(vfn, region.index, list(marked), region.anchor)
+    return vfn, vreg, implicit
+
+
+def region_params(mod: ks.Module, fn: ks.Function, region: Optional[ks.Region] = None) -> List[ks.Param]:
+    """The kernel's parameters: the function's own, the file's globals, and —
+    for a region that is not the whole function — its implicit parameters
+    (region_view)."""
     own = {p.name for p in fn.params}
-    return list(fn.params) + [p for p in global_params(mod) if p.name not in own]
+    out = list(fn.params) + [p for p in global_params(mod) if p.name not in own]
+    if region is not None and not simple_nest_function(fn, region):
+        out += region_view(mod, fn, region)[2]
+    return out
 
 
 def lower_text(text: str, function: str, fma: bool, f32: bool = False, ifconv: bool = True,
-               plain: bool = False) -> Lowered:
+               plain: bool = False, region_index: Optional[int] = None) -> Lowered:
+    """Lowers the region of `function` (the one with `region_index`, the
+    module-wide find_regions index, when the function has several)."""
     mod = ks.parse(text)
     for reg in ks.find_regions(mod):
-        if reg.function.name == function:
-            fn = ks.Function(reg.function.name, region_params(mod, reg.function), reg.function.body)
+        if reg.function.name == function and (region_index is None or reg.index == region_index):
+            fn0 = reg.function
+            if not simple_nest_function(fn0, reg):
+                fn0, reg, _ = region_view(mod, fn0, reg)
+            fn = ks.Function(fn0.name, region_params(mod, fn0), fn0.body)
             low = _Lowerer(fn, reg, fma, f32, ifconv, plain)
             low.global_scalars = {p.name for p in global_params(mod) if not p.dims}
             return low.run()
@@ -997,12 +1097,13 @@ def _scalar_struct(params, f32):
     return lines
 
 
-def gen_function(nest: str, function: str, f32: bool = False, sources: Optional[Dict[str, str]] = None
-                 ) -> Tuple[str, dict]:
-    """Device bodies of every form of one nest function.  `sources` maps each
-    form's variant (None = the original) to its module text; default: the
-    benchmark nest's text and host stage (a)'s emitted files."""
-    ns = function + ("_f32" if f32 else "")
+def gen_function(nest: str, function: str, f32: bool = False, sources: Optional[Dict[str, str]] = None,
+                 region_index: Optional[int] = None, ns_name: Optional[str] = None) -> Tuple[str, dict]:
+    """Device bodies of every form of one nest function (of its region
+    `region_index` when it has several; the struct is then named `ns_name`).
+    `sources` maps each form's variant (None = the original) to its module
+    text; default: the benchmark nest's text and host stage (a)'s emitted files."""
+    ns = (ns_name or function) + ("_f32" if f32 else "")
     texts = {}
     for form, variant, fma in FORMS:
         if sources is not None:
@@ -1010,7 +1111,7 @@ def gen_function(nest: str, function: str, f32: bool = False, sources: Optional[
             continue
         path = os.path.join(ROOT, "nests", f"{nest}.c") if variant is None else stage_a.ensure(nest, variant)
         texts[form] = (open(path).read(), fma)
-    lows = {form: lower_text(t, function, fma, f32) for form, (t, fma) in texts.items()}
+    lows = {form: lower_text(t, function, fma, f32, region_index=region_index) for form, (t, fma) in texts.items()}
     base = lows["original"]
     arrays = [p for p in base.params if p.dims]
     # merge signatures across forms (all forms must agree on static position maps)
@@ -1071,7 +1172,7 @@ def gen_function(nest: str, function: str, f32: bool = False, sources: Optional[
     # measurement baseline (acs_variant 5, ACS_ORIGINAL_NVCC): the original text
     # as nvcc compiles it by default — C operators with FMA contraction left to
     # the compiler, loads free to be cached/CSE'd.  Not bit-exact by design.
-    nv = lower_text(texts["original"][0], function, False, f32, plain=True)
+    nv = lower_text(texts["original"][0], function, False, f32, plain=True, region_index=region_index)
     lvn = ", ".join(f"const int {v}" for v in nv.loop_vars)
     L.append("// form original_nvcc: the original text, nvcc-default arithmetic (contraction allowed)")
     L.append("template <class M>")

@@ -81,6 +81,12 @@ def solve_extraction(node_class, node_cost, kid_ptr, kids, roots, time_limit_s):
         for m in members[c]:
             rows.append(r); cols.append(m); vals.append(1.0)
         lb.append(1.0); ub.append(np.inf); r += 1
+    if os.environ.get("ACS_ILP_ONE_PER_CLASS", "1") == "1":
+        for c in range(K):                # at most one node per class (some optimum has this form)
+            if len(members[c]) > 1:
+                for m in members[c]:
+                    rows.append(r); cols.append(m); vals.append(1.0)
+                lb.append(-np.inf); ub.append(1.0); r += 1
     for i in range(n):                    # a selected node needs each kid class
         for k in kids[kid_ptr[i]:kid_ptr[i + 1]]:
             for m in members[k]:

@@ -24,7 +24,8 @@ def run(exe):
 
 
 PROGRAMS = {"heat": ("main.c", "heat.c"),               # parameters, 2-D stencil, 4 calls
-            "matmul": ("main_matmul.c", "matmul_g.c")}    # file-scope arrays, inner reduction loop, branch
+            "matmul": ("main_matmul.c", "matmul_g.c"),    # file-scope arrays, inner reduction loop, branch
+            "tloop": ("main_tloop.c", "tloop.c")}         # host time loop enclosing two regions, live-in local
 
 
 @pytest.mark.parametrize("prog", sorted(PROGRAMS))
