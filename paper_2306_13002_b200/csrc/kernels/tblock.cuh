@@ -86,6 +86,8 @@ struct TbMem {
     T ym, yp;      // in-plane y-1 / y+1 neighbours held by this thread (its other cells), if hym / hyp
     bool hym, hyp; // compile-time constants once the cell loop is unrolled
     T* out;
+    T xm = T(0), xp = T(0);          // x-1 / x+1 from the adjacent lanes (warp shuffle), if hx;
+    bool hx = false, l0 = false, l31 = false;   // lanes 0 / 31 (the tile edge) read shared memory
     template <int ARR>
     using elem_t = T;
     template <int ARR, int... O>
@@ -99,6 +101,13 @@ struct TbMem {
                 if (hym) return ym;
             if constexpr (off[1] == 1 && off[2] == 0)
                 if (hyp) return yp;
+            if constexpr (off[1] == 0 && (off[2] == 1 || off[2] == -1))
+                if (hx) {
+                    constexpr int cx = off[2] * (int)sizeof(T);
+                    T v = off[2] < 0 ? xm : xp;
+                    if (off[2] < 0 ? l0 : l31) v = tb_lds(a + (unsigned)cx, T(0));
+                    return v;
+                }
             constexpr int c = (off[1] * RS + off[2]) * (int)sizeof(T);
             return tb_lds(a + (unsigned)c, T(0));
         }
@@ -131,7 +140,7 @@ struct TbGeom {
     static_assert((EX * (int)sizeof(T)) % 16 == 0, "tb2: TMA box rows are 16-byte multiples");
 };
 
-template <class NS, class T, int FORM, int TX, int TY, int NY, int PF, int MINB>
+template <class NS, class T, int FORM, int TX, int TY, int NY, int PF, int MINB, int XS>
 __global__ void __launch_bounds__(TX* TY / NY, MINB) tb2_kernel(const __grid_constant__ KernelArgs<NS> args,
                                                              const __grid_constant__ CUtensorMap rmap, int adjx,
                                                              int kchunk) {
@@ -238,6 +247,13 @@ __global__ void __launch_bounds__(TX* TY / NY, MINB) tb2_kernel(const __grid_con
                 T v = T(0);
                 TbMem<T, EX> m{sp + obox + c * EX * ES, rq[c][qm], rq[c][qc], rq[c][qn], rq[c > 0 ? c - 1 : 0][qc],
                                rq[c < NY - 1 ? c + 1 : 0][qc], c > 0, c < NY - 1, &v};
+                if constexpr (XS) {           // x neighbours from the adjacent lanes (a warp is one row)
+                    m.xm = __shfl_up_sync(0xffffffffu, rq[c][qc], 1);
+                    m.xp = __shfl_down_sync(0xffffffffu, rq[c][qc], 1);
+                    m.hx = true;
+                    m.l0 = tx == 0;
+                    m.l31 = tx == 31;
+                }
                 pt[0] = p;
                 pt[1] = y + c;
                 pt[2] = x;
@@ -267,6 +283,13 @@ __global__ void __launch_bounds__(TX* TY / NY, MINB) tb2_kernel(const __grid_con
                     // the own step-1 column of planes q-1, q, q+1 = p-2, p-1, p
                     TbMem<T, IX> m{iq + oint + c * IX * ES, sq[c][qm], sq[c][qc], sq[c][qn], sq[c > 0 ? c - 1 : 0][qc],
                                    sq[c < NY - 1 ? c + 1 : 0][qc], c > 0, c < NY - 1, &v};
+                    if constexpr (XS) {
+                        m.xm = __shfl_up_sync(0xffffffffu, sq[c][qc], 1);
+                        m.xp = __shfl_down_sync(0xffffffffu, sq[c][qc], 1);
+                        m.hx = true;
+                        m.l0 = tx == 0;
+                        m.l31 = tx == 31;
+                    }
                     pt[0] = q;
                     pt[1] = y + c;
                     pt[2] = x;
@@ -308,8 +331,9 @@ bool encode_tb_map(const LaunchReq& r, CUtensorMap& map, int& adjx) {
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <class NS, class T, int FORM, int TX, int TY, int NY, int PF, int MINB>
+template <class NS, class T, int FORM, int TX, int TY, int NY, int PF, int MINB, int XS = 0>
 acs_status launch_tb2(const LaunchReq& r) {
+    static_assert(!XS || TX == 32, "tb2: the x-shuffle needs one warp per tile row");
     static_assert(TbPlan<NS>::usable(), "tb2: not a ping-pong star stencil");
     using G = TbGeom<TX, TY, NY, PF, T>;
     KernelArgs<NS> ka;
@@ -320,7 +344,7 @@ acs_status launch_tb2(const LaunchReq& r) {
         set_error("tb2: two-step launches are not sharded");
         return ACS_E_ARG;
     }
-    auto kern = tb2_kernel<NS, T, FORM, TX, TY, NY, PF, MINB>;
+    auto kern = tb2_kernel<NS, T, FORM, TX, TY, NY, PF, MINB, XS>;
     if (r.preload) return preload_fn((const void*)kern);
     CUtensorMap map;
     int adjx = 0;
@@ -350,7 +374,7 @@ acs_status launch_tb2(const LaunchReq& r) {
 
 // the registered two-step schedules of a nest: configuration 0 is the default;
 // ACS_TB_CFG=<i> picks another one (an experiment knob for tools/gpu, not a tuning path)
-template <int TX, int TY, int NY, int PF, int MINB>
+template <int TX, int TY, int NY, int PF, int MINB, int XS = 0>
 struct TbCfg {};
 
 template <class NS, class T, int FORM, int... A>
@@ -384,10 +408,11 @@ acs_status launch_tb2_set(const LaunchReq& r) {
     return st;
 }
 
-template <int TX, int TY, int NY, int PF, int MINB>
-std::string tb2_name_of(TbCfg<TX, TY, NY, PF, MINB>) {
+template <int TX, int TY, int NY, int PF, int MINB, int XS>
+std::string tb2_name_of(TbCfg<TX, TY, NY, PF, MINB, XS>) {
     return "temporal block x2 (TMA ring, register columns), tile " + std::to_string(TX) + "x" + std::to_string(TY) +
-           ", " + std::to_string(NY) + " y-cell(s) per thread, pf " + std::to_string(PF);
+           ", " + std::to_string(NY) + " y-cell(s) per thread, pf " + std::to_string(PF) +
+           (XS ? ", x neighbours by warp shuffle" : "");
 }
 
 template <class NS, class T, class C0, class... Cs>

@@ -21,9 +21,9 @@ void register_jacobi7() {
         fill_march<gen::jacobi7, double, 0, 128, 16, 128, 4, 2>(e, 0);
         fill_march<gen::jacobi7, double, 0, 128, 4, 128, 2, 3>(e, 0);
         fill_march<gen::jacobi7, double, 0, 128, 16, 64, 4, 2, 2>(e, 0);
-        // two sweeps per launch (kernels/tblock.cuh): the default, then ACS_TB_CFG=1..4 alternatives
+        // two sweeps per launch (kernels/tblock.cuh): the default, then ACS_TB_CFG=1..5 alternatives (5: x neighbours by warp shuffle)
         fill_tb2<gen::jacobi7, double, TbCfg<32, 16, 2, 4, 4>, TbCfg<32, 16, 1, 4, 3>, TbCfg<32, 32, 2, 4, 2>,
-                 TbCfg<64, 16, 2, 4, 2>, TbCfg<32, 16, 4, 4, 4>>(e, 0);
+                 TbCfg<64, 16, 2, 4, 2>, TbCfg<32, 16, 4, 4, 4>, TbCfg<32, 16, 2, 4, 4, 1>>(e, 0);
         register_entry(&e);
     }
 }
