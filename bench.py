@@ -590,6 +590,7 @@ def per_kernel_table(peak, reps):
             # temporal blocking (two sweeps per launch, kernels/tblock.cuh): algorithmic
             # bytes as for every form (16 B/point/sweep); DRAM bytes are about half
             keys.append(("accsat", "tb2", "accsat/tb2"))
+            keys.append(("original", "tb2", "original/tb2"))
         keys = [kk for kk in keys if kk[1] is not None]
         try:
             res, w = bench_configs(kid, size, dtype, sweeps, [(v, s) for v, s, _ in keys], reps)
@@ -616,6 +617,8 @@ def per_kernel_table(peak, reps):
                 # temporal blocking vs the best single-sweep slot: same algorithmic bytes
                 # (16 B/point/sweep), about half the DRAM bytes (profiles/r02_jacobi/tb2_ncu.md)
                 row["tb2_vs_tuned"] = ratio("accsat/tb2", "accsat/tuned")
+                # saturation under temporal blocking: both forms through the same two-sweep kernel
+                row["sat_vs_orig_tb2"] = ratio("accsat/tb2", "original/tb2")
             row["bytes_per_point"] = w.bytes_per_point
         except Exception:
             pass
