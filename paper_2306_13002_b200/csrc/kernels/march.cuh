@@ -166,6 +166,9 @@ struct TmaMaps {
     // sector-aligned native row offset) is described from the aligned address
     // adjx elements earlier, so its tensor x coordinate is x + adjx
     int adjx;
+    // ring arrays read exactly once (no halo, span 1) loaded with an L2 evict_first
+    // policy (bit a); ACS_TMA_EVICT=1 turns it on (an experiment knob, tools/gpu)
+    unsigned evict;
 };
 
 // per-CTA state a body's memory policy needs
@@ -558,7 +561,10 @@ __device__ __forceinline__ void march_issue(unsigned char* slot_base, const TmaM
                     else c[d] = NS::ld_lo(A, p);
                 }
                 unsigned char* dst = P::on_ring(A) ? slot_base + P::ring_off(A) : stat + P::static_off(A);
-                tma_load<NS::ndim(A)>(dst, &maps.m[A], c, bar);
+                if ((maps.evict >> A) & 1u)
+                    tma_load_hint<NS::ndim(A)>(dst, &maps.m[A], c, bar, l2_evict_first_policy());
+                else
+                    tma_load<NS::ndim(A)>(dst, &maps.m[A], c, bar);
             }
         }
         march_issue<P, NS, A + 1>(slot_base, maps, bar, plane_base, orgx, orgy, want_static, stat);
@@ -1214,6 +1220,7 @@ bool encode_maps(const LaunchReq& r, TmaMaps<NS>& maps) {
     using P = MarchPlan<NS, T, LAYOUT, TX, TY, RX>;
     EncodeTiledFn enc = tma_encoder();
     bool first_staged = true;
+    maps.evict = 0;
     if (!enc) {
         if (acs_debug()) std::fprintf(stderr, "[acs] no cuTensorMapEncodeTiled entry point\n");
         return false;
@@ -1241,6 +1248,16 @@ bool encode_maps(const LaunchReq& r, TmaMaps<NS>& maps) {
         // one shared shift: the kernel works in tensor-map x coordinates (x + adjx)
         if (first_staged) maps.adjx = adj;
         else if (maps.adjx != adj) ACS_TMA_FAIL("staged arrays with different base shifts");
+        {
+            static const bool ev = [] {
+                const char* e = std::getenv("ACS_TMA_EVICT");
+                return e && e[0] == '1';
+            }();
+            bool once = P::on_ring(a) && P::span(a) == 1;
+            for (int p = 0; p < NS::ndim(a); ++p)
+                if (NS::ld_sig(a, p) > 0 && (NS::ld_lo(a, p) != 0 || NS::ld_hi(a, p) != 0)) once = false;
+            if (ev && once) maps.evict |= 1u << a;
+        }
         first_staged = false;
         cuuint64_t gdim[5], gstr[4];
         cuuint32_t box[5], estr[5];
