@@ -16,7 +16,8 @@
 //    unless some subscript position holds two unequal constants,
 //    ssa.cpp:63-74), same-scope identical-subscript store->load forwarding,
 //    if-φ for names the branches disagree on, conditional stores kill reuse.
-//    Regions containing inner loops are left untouched (fail-open).
+//    Sequential inner loops inside a region take for-/exit-phi leaves and
+//    start new load epochs for the bases they store (epoch kills).
 //  * Rules: FMA1-3, COMM-ADD/MUL, ASSOC-ADD1/2, ASSOC-MUL1/2
 //    (proj/src/rules.cpp:123-143) with the reference limits (10000 nodes,
 //    10 s, 10 iterations) and constant folding with host double arithmetic.
