@@ -27,10 +27,10 @@
 // un and un2 written once = 20 B/point (fp32) instead of 32.  Same generated
 // body as every skeleton: bit-exact against two step-by-step launches
 // (precondition: every rotating buffer carries the same fixed boundary).
-// Measured on B200 (profiles/r02_wave4_tb2.md): issue-bound at 139
-// instructions per point per two steps (the 2-wide halo ring adds 40 % step-1
-// work to a 19-flop body), 0.80-0.82x of two tuned single-step launches —
-// kept as an option, not the default schedule.
+// Measured on B200 (profiles/r02_wave4_tb2.md): with per-cell predicates and
+// plane pointers hoisted out of the march (139 -> 108 instructions per point
+// per two steps) it runs at 1.02-1.04x of two tuned single-step launches;
+// the 2-wide halo ring (40 % extra step-1 work) keeps it issue-bound.
 #pragma once
 
 #include <cstdlib>
@@ -186,6 +186,16 @@ __global__ void __launch_bounds__(TX* TY / NY, MINB)
     const bool ring_xy_in = rx >= lo2 && rx < hi2 && ry >= lo1 && ry < hi1;
     const bool ring_xy_arr = rx >= blo2 && rx < bhi2 && ry >= blo1 && ry < bhi1;
     const long long rgo = (long long)ry * n1 + (long long)rx * n2;
+    // hoisted per-cell predicates and plane pointers (one add per plane, no 64-bit multiplies)
+    bool own_xy_in[NY], own_xy_arr[NY];
+#pragma unroll
+    for (int c = 0; c < NY; ++c) {
+        own_xy_in[c] = x < hi2 && y + c < hi1;
+        own_xy_arr[c] = x < bhi2 && y + c < bhi1;
+    }
+    T* unp = unb + (long long)(kb - 2) * n0 + go;       // own cell 0 at plane p (starts at kb - 2)
+    T* rgp = unb + (long long)(kb - 2) * n0 + rgo;      // ring cell at plane p
+    T* u2p = un2 + (long long)(kb - 4) * n0 + go;       // own cell 0 at plane q = p - 2
 
     auto issue = [&](int a, int s) {          // TMA of plane a (u, up, vel2 boxes) into slot s
         fence_proxy_async();
@@ -266,13 +276,13 @@ __global__ void __launch_bounds__(TX* TY / NY, MINB)
                 pt[1] = y + c;
                 pt[2] = x;
                 NS::template body<FORM>(mm, args.s, pt);
-                const bool in = pin && x < hi2 && y + c < hi1;
+                const bool in = pin && own_xy_in[c];
                 T s1 = v;
                 if (!in) {                    // the un buffer's value: what step 2 would read there
                     s1 = T(0);
-                    if (parr && x < bhi2 && y + c < bhi1) s1 = unb[(long long)p * n0 + go + c * n1];
+                    if (parr && own_xy_arr[c]) s1 = unp[c * n1];
                 } else if (pstore) {
-                    unb[(long long)p * n0 + go + c * n1] = v;
+                    unp[c * n1] = v;
                 }
                 sq[c][u] = s1;
                 tb_sts(s1p + oe + c * IX * ES, s1);
@@ -291,7 +301,7 @@ __global__ void __launch_bounds__(TX* TY / NY, MINB)
                 T s1 = v;
                 if (!(pin && ring_xy_in)) {
                     s1 = T(0);
-                    if (parr && ring_xy_arr) s1 = unb[(long long)p * n0 + rgo];
+                    if (parr && ring_xy_arr) s1 = *rgp;
                 }
                 tb_sts(s1p + re, s1);
             }
@@ -313,9 +323,12 @@ __global__ void __launch_bounds__(TX* TY / NY, MINB)
                     pt[1] = y + c;
                     pt[2] = x;
                     NS::template body<FORM>(mm, args.s, pt);
-                    if (x < hi2 && y + c < hi1) un2[(long long)q * n0 + go + c * n1] = v;
+                    if (own_xy_in[c]) u2p[c * n1] = v;
                 }
             }
+            unp += n0;
+            rgp += n0;
+            u2p += n0;
         }
     }
 }
@@ -400,9 +413,9 @@ acs_status launch_tbw(const LaunchReq& r) {
     set_smem_attr_once(kern, G::smem, attr_done);
     const long long nx = ka.hi[2] - ka.lo[2], ny = ka.hi[1] - ka.lo[1], nz = ka.hi[0] - ka.lo[0];
     const long long tiles = ((nx + TX - 1) / TX) * ((ny + TY - 1) / TY);
-    // 128-plane chunks (measured best of 64 / 128 / 256 / whole column at 1024^3,
+    // 96-plane chunks (measured best of 64 / 80 / 96 / 128 / 192 / 256 at 1024^3,
     // profiles/r02_wave4_tb2.md); never below 24 (6 extra planes per chunk)
-    long long kchunk = 128;
+    long long kchunk = 96;
     (void)tiles;
     static const long long kch_env = [] {   // experiment knob (tools/gpu), not a tuning path
         const char* e = std::getenv("ACS_TB_KCHUNK");

@@ -390,7 +390,7 @@ def test_temporal_blocking_equals_step_by_step(size, nsteps, variant):
     assert bitwise_equal(got, g[newest]), f"{size} x{nsteps}"
 
 
-@pytest.mark.parametrize("size", [(6, 7, 13), (21, 9, 70), (33, 47, 130), (70, 40, 37)])
+@pytest.mark.parametrize("size", [(6, 7, 13), (21, 9, 70), (33, 47, 130), (70, 40, 37), (230, 12, 37)])
 @pytest.mark.parametrize("nsteps", [2, 4, 6])
 @pytest.mark.parametrize("variant", ["original", "accsat"])
 def test_wave4_leapfrog2_equals_step_by_step(size, nsteps, variant):
