@@ -491,6 +491,55 @@ def tune_kernel(kid, size, dtype, variant):
     return best, name, ms
 
 
+def bench_leapfrog2(kid, size, dtype, variant, slot, reps, steps=12, warmup=2):
+    """wave4's two-step launch (acs_launch_leapfrog2: step 2 into a fourth buffer,
+    4-buffer rotation) against the given single-step slot on the same resident
+    arrays, `steps` time steps per timed sample, samples interleaved; median and
+    IQR of ms per time step, GB/s of the algorithmic bytes (16 B/point/step)."""
+    import torch
+    from paper_2306_13002_b200 import backend, nests
+    w = nests.workload(kid, size, dtype=dtype)
+    k = backend.Kernel.lookup(kid)
+    arrs = nests.device_inputs(w, native=True, kernel=k)
+    x = backend.empty_native(k, "un", tuple(arrs["un"].shape), arrs["un"].dtype)
+    sc = dict(w.scalars)
+    names = list(arrs)
+
+    def single():
+        for t in range(steps):
+            roles = nests.role_buffers(w.spec.nest, names, t)
+            k.launch({p: arrs[r] for p, r in roles.items()}, sc, variant, slot)
+
+    def blocked():
+        b = {"u": arrs["u"], "up": arrs["up"], "un": arrs["un"], "x": x}
+        for _ in range(steps // 2):
+            k.launch_leapfrog2({"u": b["u"], "up": b["up"], "un": b["un"], "vel2": arrs["vel2"]}, b["x"], sc, variant)
+            b = {"u": b["x"], "up": b["un"], "un": b["up"], "x": b["u"]}
+
+    fns = [single, blocked]
+    for _ in range(warmup):
+        for f in fns:
+            f()
+    torch.cuda.synchronize()
+    ev = [[] for _ in fns]
+    for _ in range(reps):
+        for i, f in enumerate(fns):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            f()
+            b.record()
+            ev[i].append((a, b))
+    torch.cuda.synchronize()
+    out = []
+    for i in range(len(fns)):
+        med, iqr = stats([a.elapsed_time(b) / steps for a, b in ev[i]])
+        out.append({"ms": round(med, 4), "iqr_ms": round(iqr, 4),
+                    "gbs": round(w.algorithmic_bytes / (med * 1e-3) / 1e9, 1)})
+    del arrs, x
+    torch.cuda.empty_cache()
+    return out
+
+
 def bench_configs(kid, size, dtype, sweeps, configs, reps, warmup=3):
     """Device-resident GB/s of one nest at its BASELINE size for several
     (form, schedule) configurations, each on its own resident arrays, with the
@@ -622,6 +671,19 @@ def per_kernel_table(peak, reps):
             row["bytes_per_point"] = w.bytes_per_point
         except Exception:
             pass
+        if fn == "wave4" and slots.get("accsat") is not None:
+            # two leapfrog steps per launch (kernels/tbwave.cuh) vs the tuned single step,
+            # interleaved on the same arrays; algorithmic bytes as for every form
+            try:
+                single, blocked = bench_leapfrog2(kid, size, dtype, "accsat", slots["accsat"], max(7, reps // 3))
+                blocked["frac"] = round(blocked["gbs"] / peak, 4)
+                row["accsat/tb2"] = blocked
+                row["accsat/tuned_vs_tb2_same_run"] = single
+                band = blocked["iqr_ms"] / blocked["ms"] + single["iqr_ms"] / single["ms"]
+                row["tb2_vs_tuned"] = {"ratio": round(single["ms"] / blocked["ms"], 3), "noise_band": round(band, 4),
+                                       "not_slower": single["ms"] / blocked["ms"] >= 1 - band}
+            except Exception as e:  # report, never hide
+                row["tb2_error"] = str(e)[:300]
         mix = MIX.get(fn)
         if mix and mix in mixpk and "accsat/tuned" in row and "gbs" in row["accsat/tuned"]:
             row["mix"] = f"{mix[0]}R:{mix[1]}W"
